@@ -1,0 +1,138 @@
+/*
+ * rtgpu.h -- C-ABI of the B200 batched RTGPU schedulability engine.
+ *
+ * This is the drop-in boundary for the data-parallel hot path of the
+ * reference package `gpusched` (reference: pkg/src/gpusched/).  The
+ * reference is pure Python, so "its FFI" is the ctypes binding its public
+ * API would use; INTEGRATION.md shows that binding.  Every entry point is
+ * plain C: int64/int32 pointers and sizes, no torch or CUDA types.
+ *
+ *   reference function (file:line)                     replaced by
+ *   -----------------------------------------------    -------------------------
+ *   analysis.analyze_rtgpu            analysis.py:275  rtgpu_analyze_{host,device}
+ *   analysis._grid_search             analysis.py:250    (method RTGPU_METHOD_RTGPU)
+ *   analysis._min_feasible_gn         analysis.py:239
+ *   gpu.feasible_allocations          gpu.py:69
+ *   gpu.gpu_bounds_cache              gpu.py:91
+ *   gpu.gpu_response_bounds           gpu.py:25
+ *   analysis.mem_response             analysis.py:156
+ *   analysis.cpu_response             analysis.py:175
+ *   analysis.end_to_end               analysis.py:191
+ *   analysis.{mem,cpu}_workload       analysis.py:109,118
+ *   analysis.{mem,cpu}_inter_arrival  analysis.py:57,89
+ *   suspension.chain_workload         suspension.py:77
+ *   suspension.fixed_point            suspension.py:123
+ *   analysis.analyze_self_suspension_baseline  analysis.py:319  (RTGPU_METHOD_SELFSUSP)
+ *   analysis.analyze_busy_waiting_baseline     analysis.py:355  (RTGPU_METHOD_BUSYWAIT)
+ *   suspension.{workload,max_workload,         suspension.py:107-176
+ *               segment_response,task_response}   rtgpu_susp_{host,device}
+ *
+ * ---------------------------------------------------------------------
+ * Packed task-set layout ("blob"), shared by the engine and the oracle.
+ * ---------------------------------------------------------------------
+ * A batch is a flat int64 array holding S blobs back to back; set_off[s]
+ * is the word offset of blob s (set_off[S] = total words) and
+ * task_base[s] the index of its first task in the per-task result arrays
+ * (task_base[S] = total tasks).  Every duration is an integer count of
+ * "input ticks" (1 tick = 1/time_scale us; the engine is scale free, the
+ * host multiplies result denominators by time_scale).
+ *
+ *   header (RTGPU_HDR_WORDS):
+ *     [0] n_tasks  [1] physical_sms (GN)  [2] mem_model (0 two_copy, 1 one_copy)
+ *     [3] alpha_den (A: interleave ratio = alpha_num / A)  [4] blob words
+ *     [5] max m over tasks  [6] max p over tasks  [7] 0
+ *   n task records (RTGPU_TASK_WORDS each), in TaskSet.by_priority() order:
+ *     [0] m (CPU segments)  [1] p (memory segments)  [2] D  [3] T
+ *     [4] priority  [5] seg_off (word offset of the segment area from the
+ *     blob start)  [6] index of the task in TaskSet.tasks  [7] 0
+ *   segment area of a task (g = m - 1 GPU segments):
+ *     cl_lo[m] cl_hi[m] ml_lo[p] ml_hi[p] gw_lo[g] gw_hi[g] gl[g] alpha_num[g]
+ *
+ * Results (per set s / per task t / per blob word w):
+ *   status[s]   RTGPU_* status below
+ *   evals[s]    number of task evaluations the search performed
+ *   vsm[t]      virtual SMs (2*GN_i) of the reported allocation, 0 if none
+ *   e2e_num[t]  end-to-end bound numerator; RTGPU_NONE if the analysis
+ *               returned None, RTGPU_ABSENT if the task is not in per_task
+ *   den[t]      denominator (in input ticks) shared by all values of task t
+ *   detail[w]   optional, same shape as the blob buffer: at the task's
+ *               segment area, the cl_lo slots hold cpu_r_up[m], the ml_lo
+ *               slots mem_r_up[p], the gw_lo / gw_hi slots the GPU response
+ *               bounds GR lo / hi; numerators over den[t], RTGPU_NONE = None.
+ */
+#ifndef RTGPU_H
+#define RTGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTGPU_ABI_VERSION 1
+
+#define RTGPU_HDR_WORDS 8
+#define RTGPU_TASK_WORDS 8
+
+#define RTGPU_TWO_COPY 0
+#define RTGPU_ONE_COPY 1
+
+/* analysis methods (model.AnalysisMethod) */
+#define RTGPU_METHOD_RTGPU 0
+#define RTGPU_METHOD_SELFSUSP 1
+#define RTGPU_METHOD_BUSYWAIT 2
+
+/* per-set status */
+#define RTGPU_UNSCHEDULABLE 0
+#define RTGPU_SCHEDULABLE 1
+#define RTGPU_UNDECIDED 2  /* allocation search exceeded eval_budget         */
+#define RTGPU_RANGE 3      /* exact values exceed the 127-bit range          */
+#define RTGPU_INVALID 4    /* input the reference rejects with an exception  */
+
+/* sentinels in e2e_num / detail */
+#define RTGPU_NONE (-1LL)
+#define RTGPU_ABSENT (-2LL)
+
+/* flags */
+#define RTGPU_F_BOUNDS 1u  /* fill e2e_num/den for the reported allocation   */
+#define RTGPU_F_DETAIL 2u  /* also the per-segment report (implies BOUNDS)   */
+
+/* limits of the engine (checked on entry; larger sets -> RTGPU_INVALID) */
+#define RTGPU_MAX_TASKS 64
+#define RTGPU_MAX_M 16
+
+int rtgpu_abi_version(void);
+const char *rtgpu_last_error(void);
+/* number of visible CUDA devices, SM count and compute capability of device 0 */
+int rtgpu_device_info(int *n_devices, int *sm_count, int *cc_major, int *cc_minor);
+
+/*
+ * Batched allocation search + response-time analysis (Algorithm 2) of S
+ * packed task sets, each exactly as gpusched.analysis.analyze(ts, method).
+ * Host pointers: the call copies the batch to the current device, runs the
+ * kernels and copies the results back (the end-to-end path).
+ * eval_budget <= 0 means unlimited.  Returns 0 or a negative error code.
+ */
+int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off,
+                       const int64_t *task_base, int64_t n_sets, int method,
+                       unsigned flags, int64_t eval_budget, int32_t *status,
+                       int64_t *evals, int32_t *vsm, int64_t *e2e_num,
+                       int64_t *den, int64_t *detail);
+
+/* Same on device-resident buffers, enqueued on `stream` (cudaStream_t or
+ * NULL for the legacy default stream).  Asynchronous. */
+int rtgpu_analyze_device(const int64_t *d_blobs, const int64_t *d_set_off,
+                         const int64_t *d_task_base, int64_t n_sets,
+                         int method, unsigned flags, int64_t eval_budget,
+                         int32_t *d_status, int64_t *d_evals, int32_t *d_vsm,
+                         int64_t *d_e2e_num, int64_t *d_den,
+                         int64_t *d_detail, void *stream);
+
+/* number of kernel launches the last rtgpu_analyze_* call enqueued */
+int64_t rtgpu_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTGPU_H */

@@ -1,0 +1,241 @@
+"""Packing of TaskSets into the engine's int64 blob layout and unpacking of
+engine results into ``AnalysisReport`` objects.
+
+The layout is documented in ``include/rtgpu.h``.  Every exact rational of a
+task set is brought to integers with one per-set time scale S (lcm of all
+duration denominators, normally 1 for integer-microsecond tasksets) and one
+interleave-ratio denominator A (lcm of the ratio denominators, normally a
+divisor of 100).  The engine returns numerator / denominator pairs in input
+ticks; dividing by S gives microseconds again, so results are bit-exact
+Fractions, not floats.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from fractions import Fraction
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .model import (
+    AnalysisMethod,
+    AnalysisReport,
+    ExecBounds,
+    MemModel,
+    SmAllocation,
+    TaskReport,
+    TaskSet,
+    expected_mem_count,
+)
+
+HDR_WORDS = 8
+TASK_WORDS = 8
+MAX_TASKS = 64
+MAX_M = 16
+INT64_MAX = (1 << 63) - 1
+
+# status codes (include/rtgpu.h)
+UNSCHEDULABLE, SCHEDULABLE, UNDECIDED, RANGE, INVALID = 0, 1, 2, 3, 4
+NONE, ABSENT = -1, -2
+METHOD_CODES = {AnalysisMethod.RTGPU: 0, AnalysisMethod.SELF_SUSPENSION: 1,
+                AnalysisMethod.BUSY_WAITING: 2}
+F_BOUNDS, F_DETAIL = 1, 2
+
+
+class EngineRangeError(ArithmeticError):
+    """The exact values of a task set exceed the engine's integer range."""
+
+
+@dataclass
+class SetMeta:
+    """What the unpacker needs to turn engine output back into a report."""
+
+    ts: TaskSet
+    order: tuple  # TaskSpec objects in by_priority() order (blob order)
+    time_scale: int
+    word_off: int
+    task_base: int
+
+
+@dataclass
+class PackedBatch:
+    blobs: np.ndarray      # int64 [W]
+    set_off: np.ndarray    # int64 [S + 1]
+    task_base: np.ndarray  # int64 [S + 1]
+    metas: list
+
+    @property
+    def n_sets(self) -> int:
+        return len(self.metas)
+
+
+def _lcm_all(values) -> int:
+    out = 1
+    for v in values:
+        out = out * v // math.gcd(out, v)
+    return out
+
+
+def _durations(ts: TaskSet):
+    for t in ts.tasks:
+        yield t.deadline
+        yield t.period
+        for b in t.cpu_segments:
+            yield b.lo
+            yield b.hi
+        for b in t.mem_segments:
+            yield b.lo
+            yield b.hi
+        for g in t.gpu_segments:
+            yield g.work.lo
+            yield g.work.hi
+            yield g.critical_path_overhead
+
+
+def _check_shape(ts: TaskSet) -> None:
+    if len(ts.tasks) > MAX_TASKS:
+        raise ValueError(f"engine supports at most {MAX_TASKS} tasks per set")
+    for t in ts.tasks:
+        m = len(t.cpu_segments)
+        if not 1 <= m <= MAX_M:
+            raise ValueError(f"task {t.id}: engine supports 1..{MAX_M} CPU segments")
+        if len(t.gpu_segments) != m - 1:
+            raise ValueError(f"task {t.id}: gpu segment count != {m - 1}")
+        want = expected_mem_count(m, ts.mem_model)
+        if len(t.mem_segments) != want:
+            raise ValueError(f"task {t.id}: mem segment count != {want}")
+
+
+def pack_set(ts: TaskSet) -> tuple[list[int], int, tuple]:
+    """One blob as a list of Python ints plus its time scale and task order."""
+    _check_shape(ts)
+    S = _lcm_all(Fraction(d).denominator for d in _durations(ts))
+    A = _lcm_all(Fraction(g.interleave_ratio).denominator
+                 for t in ts.tasks for g in t.gpu_segments)
+    order = ts.by_priority()
+    index_of = {id(t): i for i, t in enumerate(ts.tasks)}
+    n = len(order)
+
+    def tick(x) -> int:
+        v = Fraction(x) * S
+        assert v.denominator == 1
+        return int(v)
+
+    header = [n, ts.platform.physical_sms,
+              0 if ts.mem_model is MemModel.TWO_COPY else 1, A, 0,
+              max((len(t.cpu_segments) for t in order), default=0),
+              max((len(t.mem_segments) for t in order), default=0), 0]
+    records: list[int] = []
+    segs: list[int] = []
+    seg_base = HDR_WORDS + TASK_WORDS * n
+    for t in order:
+        m, p = len(t.cpu_segments), len(t.mem_segments)
+        records += [m, p, tick(t.deadline), tick(t.period), t.priority,
+                    seg_base + len(segs), index_of[id(t)], 0]
+        segs += [tick(b.lo) for b in t.cpu_segments]
+        segs += [tick(b.hi) for b in t.cpu_segments]
+        segs += [tick(b.lo) for b in t.mem_segments]
+        segs += [tick(b.hi) for b in t.mem_segments]
+        segs += [tick(g.work.lo) for g in t.gpu_segments]
+        segs += [tick(g.work.hi) for g in t.gpu_segments]
+        segs += [tick(g.critical_path_overhead) for g in t.gpu_segments]
+        for g in t.gpu_segments:
+            a = Fraction(g.interleave_ratio) * A
+            segs.append(int(a))
+    blob = header + records + segs
+    blob[4] = len(blob)
+    for v in blob:
+        if not -INT64_MAX <= v <= INT64_MAX:
+            raise EngineRangeError("task set values exceed int64 after scaling")
+    return blob, S, order
+
+
+def pack_tasksets(tasksets: Sequence[TaskSet]) -> PackedBatch:
+    words: list[int] = []
+    set_off = [0]
+    task_base = [0]
+    metas = []
+    for ts in tasksets:
+        blob, S, order = pack_set(ts)
+        metas.append(SetMeta(ts, order, S, len(words), task_base[-1]))
+        words += blob
+        set_off.append(len(words))
+        task_base.append(task_base[-1] + len(order))
+    return PackedBatch(np.asarray(words, dtype=np.int64).reshape(-1),
+                       np.asarray(set_off, dtype=np.int64),
+                       np.asarray(task_base, dtype=np.int64), metas)
+
+
+@dataclass
+class RawResults:
+    status: np.ndarray   # int32 [S]
+    evals: np.ndarray    # int64 [S]
+    vsm: np.ndarray      # int32 [T]
+    e2e_num: np.ndarray  # int64 [T]
+    den: np.ndarray      # int64 [T]
+    detail: Optional[np.ndarray]  # int64 [W] or None
+
+    @classmethod
+    def empty(cls, batch: PackedBatch, detail: bool) -> "RawResults":
+        S = batch.n_sets
+        T = int(batch.task_base[-1])
+        return cls(np.zeros(S, np.int32), np.zeros(S, np.int64), np.zeros(T, np.int32),
+                   np.zeros(T, np.int64), np.ones(T, np.int64),
+                   np.zeros(len(batch.blobs), np.int64) if detail else None)
+
+
+def _val(num: int, den: int, S: int) -> Optional[Fraction]:
+    if num == NONE:
+        return None
+    return Fraction(int(num), int(den) * S)
+
+
+def unpack_report(batch: PackedBatch, res: RawResults, s: int,
+                  method: AnalysisMethod) -> AnalysisReport:
+    """AnalysisReport of set s, shaped exactly like the reference's."""
+    meta: SetMeta = batch.metas[s]
+    st = int(res.status[s])
+    if st == INVALID:
+        raise ValueError("critical-path overhead exceeds inflated work "
+                         "(or a task set the reference cannot analyse)")
+    if st == RANGE:
+        raise EngineRangeError("exact values of this task set exceed the 127-bit range")
+    if st == UNDECIDED:
+        raise TimeoutError("allocation search exceeded its evaluation budget")
+    S = meta.time_scale
+    tb = meta.task_base
+    allocation = None
+    if st == SCHEDULABLE:
+        by_id = {t.id: int(res.vsm[tb + i]) for i, t in enumerate(meta.order)}
+        gpu_ids = [t.id for t in meta.order if t.gpu_segments]
+        pure_ids = [t.id for t in meta.ts.tasks if not t.gpu_segments]
+        allocation = SmAllocation({**{i: by_id[i] for i in gpu_ids},
+                                   **{i: 0 for i in pure_ids}})
+    per_task: dict[str, TaskReport] = {}
+    for i, t in enumerate(meta.order):
+        num = int(res.e2e_num[tb + i])
+        if num == ABSENT:
+            continue
+        den = int(res.den[tb + i])
+        e2e = _val(num, den, S)
+        gpu_r: tuple = ()
+        mem_r: tuple = ()
+        cpu_r: tuple = ()
+        if res.detail is not None:
+            rec = batch.blobs[meta.word_off + HDR_WORDS + TASK_WORDS * i:
+                              meta.word_off + HDR_WORDS + TASK_WORDS * (i + 1)]
+            m, p = int(rec[0]), int(rec[1])
+            g = m - 1
+            base = meta.word_off + int(rec[5])
+            d = res.detail[base: base + 2 * m + 2 * p + 4 * g]
+            gl = d[2 * m + 2 * p: 2 * m + 2 * p + g]
+            gh = d[2 * m + 2 * p + g: 2 * m + 2 * p + 2 * g]
+            gpu_r = tuple(ExecBounds(_val(int(a), den, S), _val(int(b), den, S))
+                          for a, b in zip(gl, gh))
+            if method is AnalysisMethod.RTGPU:
+                mem_r = tuple(_val(int(x), den, S) for x in d[2 * m: 2 * m + p])
+                cpu_r = tuple(_val(int(x), den, S) for x in d[:m])
+        per_task[t.id] = TaskReport(gpu_r=gpu_r, mem_r_up=mem_r, cpu_r_up=cpu_r,
+                                    end_to_end_up=e2e)
+    return AnalysisReport(st == SCHEDULABLE, method, allocation, per_task)
