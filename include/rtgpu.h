@@ -120,9 +120,12 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off,
                        int64_t *den, int64_t *detail);
 
 /* Same on device-resident buffers, enqueued on `stream` (cudaStream_t or
- * NULL for the legacy default stream).  Asynchronous. */
+ * NULL for the legacy default stream).  Asynchronous.  max_tasks / max_m /
+ * max_p bound n, m and p over the batch (they size shared memory; a set
+ * exceeding them reports RTGPU_INVALID). */
 int rtgpu_analyze_device(const int64_t *d_blobs, const int64_t *d_set_off,
                          const int64_t *d_task_base, int64_t n_sets,
+                         int max_tasks, int max_m, int max_p,
                          int method, unsigned flags, int64_t eval_budget,
                          int32_t *d_status, int64_t *d_evals, int32_t *d_vsm,
                          int64_t *d_e2e_num, int64_t *d_den,

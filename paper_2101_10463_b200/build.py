@@ -1,0 +1,63 @@
+"""In-tree build of the native library (CUDA kernels for sm_100a + host code).
+
+    python -m paper_2101_10463_b200.build
+
+produces paper_2101_10463_b200/librtgpu.so.  Nothing is JIT-compiled at
+import time; the package refuses to run without this library.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "librtgpu.so")
+SOURCES = ["rtgpu_engine.cu", "rtgpu_k_f64.cu", "rtgpu_k_i64.cu", "rtgpu_k_i128.cu",
+           "taskgen.cpp"]
+HEADERS = ["engine_core.cuh", "kernel.cuh"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+         "-I", os.path.join(ROOT, "include")]
+OBJDIR = os.path.join(HERE, "build")
+
+
+def _inputs():
+    out = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    out += [os.path.join(ROOT, "include", h) for h in ("rtgpu.h", "rtgpu_gen.h")]
+    return out
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    return all(os.path.getmtime(p) <= t for p in _inputs())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return LIB
+    os.makedirs(OBJDIR, exist_ok=True)
+    procs, objs = [], []
+    for src in SOURCES:  # one translation unit per arithmetic: compile in parallel
+        obj = os.path.join(OBJDIR, src + ".o")
+        objs.append(obj)
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((cmd, subprocess.Popen(cmd, cwd=CSRC)))
+    for cmd, pr in procs:
+        if pr.wait() != 0:
+            raise RuntimeError("build failed: " + " ".join(cmd))
+    link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
+    subprocess.run(link, check=True, cwd=CSRC)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,1018 @@
+/*
+ * engine_core.cuh -- the RTGPU analysis of one packed task set, written once
+ * for a cooperating "team": a 32-lane warp on sm_100a (WarpTeam, the
+ * product) or a sequential emulation of the same lanes (SeqTeam, used only by
+ * the test harness in tests/ to check the logic on a CPU-only box).
+ *
+ * What is computed: exactly gpusched.analysis.analyze(ts, RTGPU) -- verdict,
+ * the lexicographically first schedulable SM allocation of Algorithm 2
+ * (reference analysis.py:250 _grid_search over gpu.py:69
+ * feasible_allocations) and, on request, the report bounds.
+ *
+ * How (DESIGN.md section 3 has the proofs):
+ *  - Exact arithmetic.  For a given prefix of the allocation every value is a
+ *    rational with denominator dividing Q = 2*lcm(GN_i)*[A*GN_k]; the warp
+ *    scales inputs by Q and computes in V = double (integer-valued, exact
+ *    below 2^52), int64 or int128.  A set whose range does not fit V is
+ *    escalated to the next V by the host driver, never approximated.
+ *  - Chain workload W_i^h(t) (suspension.py:77) in O(p): prefix sums of
+ *    segment+gap over one job, a floor-division jump over whole periods
+ *    (one steady period is exactly the cycle length C), and the final
+ *    partial period.  Lanes own (task i, start segment h) pairs; max over h
+ *    and sum over hp(k) are warp shuffles.
+ *  - Fixed points (suspension.py:123) iterate from below with two exact
+ *    accelerations that cannot skip the least fixed point: warm starts from
+ *    the fixed point of a smaller base, and a slope-1 jump (a maximising
+ *    walk still inside a segment keeps the interference growing at slope 1,
+ *    so no fixed point lies within its remaining length).
+ *  - Allocation search.  Task k's verdict depends only on the SM counts of
+ *    tasks before it in priority order (prefix property) and is monotone in
+ *    its own count (Lemma 4 bound shrinks with GN_k).  When no gap can go
+ *    negative ("regular" sets -- every validated set), interference is also
+ *    monotone in the hp counts, so the first schedulable allocation in
+ *    lexicographic order is the greedy one: each task takes the smallest
+ *    passing count, found by bisection.  Irregular sets run an exact
+ *    depth-first search with prefix pruning under an evaluation budget.
+ */
+#pragma once
+#include <stdint.h>
+
+#include "../../include/rtgpu.h"
+
+#ifdef __CUDACC__
+#define RT_HD __host__ __device__ inline
+#else
+#define RT_HD inline
+#endif
+
+namespace rtgpu {
+
+typedef long long i64;
+typedef __int128 i128;
+
+enum { K_CPU = 0, K_MEM = 1 };
+
+/* internal status: range exceeded for this arithmetic -> escalate */
+enum { ST_ESCALATE = 99 };
+
+static const int ITER_CAP = 1 << 22; /* safety net per fixed point */
+
+/* ------------------------------------------------------------ arithmetic */
+
+template <class V> struct Num;
+
+template <> struct Num<double> {
+    typedef i64 Qt;
+    static RT_HD i64 limit() { return (i64)1 << 52; }
+    static RT_HD double sc(i64 x, i64 q) { return (double)(x * q); }
+    static RT_HD double of(i64 x) { return (double)x; }
+    static RT_HD double floordiv(double a, double b) {
+        double q = floor(a / b);
+        if (q * b > a) q -= 1.0;
+        else if ((q + 1.0) * b <= a) q += 1.0;
+        return q;
+    }
+    static RT_HD i128 wide(double v) { return (i128)(i64)v; }
+};
+
+template <> struct Num<i64> {
+    typedef i64 Qt;
+    static RT_HD i64 limit() { return (i64)1 << 62; }
+    static RT_HD i64 sc(i64 x, i64 q) { return x * q; }
+    static RT_HD i64 of(i64 x) { return x; }
+    static RT_HD i64 floordiv(i64 a, i64 b) { return a / b; }
+    static RT_HD i128 wide(i64 v) { return (i128)v; }
+};
+
+template <> struct Num<i128> {
+    typedef i128 Qt;
+    static RT_HD i128 limit() { return (i128)1 << 125; }
+    static RT_HD i128 sc(i64 x, i128 q) { return (i128)x * q; }
+    static RT_HD i128 of(i64 x) { return (i128)x; }
+    static RT_HD i128 floordiv(i128 a, i128 b) { return a / b; }
+    static RT_HD i128 wide(i128 v) { return v; }
+};
+
+template <class T> RT_HD T tmax(T a, T b) { return a > b ? a : b; }
+template <class T> RT_HD T tmin(T a, T b) { return a < b ? a : b; }
+
+template <class T> RT_HD T gcdq(T a, T b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b != 0) {
+        T t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+/* lcm with overflow detection against lim; returns 0 on overflow */
+template <class T> RT_HD T lcm_lim(T a, T b, T lim) {
+    T g = gcdq(a, b);
+    T a1 = a / g;
+    if (a1 > lim / b) return 0;
+    return a1 * b;
+}
+
+/* ------------------------------------------------------------ per-task data */
+
+struct TaskRec {
+    i64 D, T, prio, seg;
+    i64 sClu, sCll, sMlu, sMll, sGWlo, sInfl, sGL, innerCll, maxMlu, B;
+    int m, p, gmin, g;
+    int isgpu, flags, idx, pad;
+};
+
+enum { TF_INV = 1, TF_ISOFAIL = 2, TF_IRREG = 4, TF_UNSUP = 8 };
+
+/* Sizes of the per-warp shared-memory slab for a batch whose sets have at
+ * most maxn tasks, MC CPU and MP memory segments per task. */
+struct Dims {
+    int maxn, MC, MP;
+};
+
+template <class V> struct Layout {
+    int SC, SM;        /* view stride (in V) per task for CPU / memory chains */
+    int off_views_c;   /* byte offsets inside the slab */
+    int off_views_m;
+    int off_scr;
+    int scr_n;         /* scratch V entries */
+    int bytes;
+    RT_HD void init(const Dims &d) {
+        SC = 3 * d.MC + 4;
+        SM = d.MP > 0 ? 3 * d.MP + 4 : 0;
+        int o = (int)sizeof(TaskRec) * d.maxn;
+        o = (o + 15) & ~15;
+        off_views_c = o;
+        o += (int)sizeof(V) * SC * d.maxn;
+        off_views_m = o;
+        o += (int)sizeof(V) * SM * d.maxn;
+        off_scr = o;
+        scr_n = 2 * (d.MP + d.MC + 2) + d.MP + 3 * d.MC;
+        o += (int)sizeof(V) * scr_n;
+        bytes = (o + 15) & ~15;
+    }
+};
+
+/* view offsets inside one task's chain view */
+struct VOff {
+    int e, P, EP, F1, WN;
+    RT_HD VOff(int p_max) : e(0), P(p_max), EP(2 * p_max + 1), F1(3 * p_max + 2), WN(3 * p_max + 3) {}
+};
+
+/* ------------------------------------------------------------ set context */
+
+template <class V> struct SetCtx {
+    typedef typename Num<V>::Qt Qt;
+    const i64 *blob; /* global: this set's blob */
+    TaskRec *tr;
+    V *vc, *vm, *scr;
+    Layout<V> L;
+    int n, GN, mm;
+    i64 A;
+    int maxn, MC, MP, GC, GM; /* batch maxima, lane group sizes */
+    i64 Vb;             /* range bound in input ticks */
+    Qt qlim;            /* largest admissible scale: limit / Vb */
+    /* current views: tasks [0, vn) at scale vq */
+    int vn;
+    Qt vq;
+    int esc;            /* range exceeded -> escalate */
+    int stuck;          /* fixed point iteration cap hit */
+    i64 evals, budget;
+    int budget_hit;
+};
+
+/* ------------------------------------------------------------ teams */
+
+template <class V> struct WRE { V w, rho; };
+
+#ifdef __CUDACC__
+template <class V> __device__ __forceinline__ V shfl_x(V v, int off) {
+    return __shfl_xor_sync(0xffffffffu, v, off);
+}
+template <> __device__ __forceinline__ i128 shfl_x<i128>(i128 v, int off) {
+    unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+    lo = __shfl_xor_sync(0xffffffffu, lo, off);
+    hi = __shfl_xor_sync(0xffffffffu, hi, off);
+    return (i128)(((unsigned __int128)hi << 64) | lo);
+}
+
+struct WarpTeam {
+    int lane;
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+    __device__ __forceinline__ bool leader() const { return lane == 0; }
+    template <class F> __device__ __forceinline__ void pfor(int n, F f) const {
+        for (int i = lane; i < n; i += 32) f(i);
+        __syncwarp();
+    }
+    __device__ __forceinline__ bool any(bool b) const { return __any_sync(0xffffffffu, b); }
+    /* slot = lane; f(slot, w, rho, err).  Max (w, then rho) within groups of
+     * G lanes, then sum of w and max of rho across groups. */
+    template <class V, class F>
+    __device__ __forceinline__ void group_reduce(int G, F f, V &wsum, V &rhomax, bool &err) const {
+        V w = 0, rho = 0;
+        bool e = false;
+        f(lane, w, rho, e);
+        for (int off = 1; off < G; off <<= 1) {
+            V w2 = shfl_x(w, off), r2 = shfl_x(rho, off);
+            if (w2 > w || (w2 == w && r2 > rho)) {
+                w = w2;
+                rho = r2;
+            }
+        }
+        for (int off = G; off < 32; off <<= 1) {
+            w += shfl_x(w, off);
+            V r2 = shfl_x(rho, off);
+            if (r2 > rho) rho = r2;
+        }
+        wsum = w;
+        rhomax = rho;
+        err = __any_sync(0xffffffffu, e);
+    }
+};
+#endif
+
+/* Sequential emulation of the warp (test harness only). */
+struct SeqTeam {
+    RT_HD void sync() const {}
+    RT_HD bool leader() const { return true; }
+    template <class F> RT_HD void pfor(int n, F f) const {
+        for (int i = 0; i < n; i++) f(i);
+    }
+    RT_HD bool any(bool b) const { return b; }
+    template <class V, class F> RT_HD void group_reduce(int G, F f, V &wsum, V &rhomax, bool &err) const {
+        V ws = 0, rm = 0;
+        bool e = false;
+        for (int g0 = 0; g0 < 32; g0 += G) {
+            V bw = 0, br = 0;
+            for (int s = g0; s < g0 + G; s++) {
+                V w = 0, rho = 0;
+                bool es = false;
+                f(s, w, rho, es);
+                e = e || es;
+                if (s == g0 || w > bw || (w == bw && rho > br)) {
+                    bw = w;
+                    br = rho;
+                }
+            }
+            ws += bw;
+            if (br > rm) rm = br;
+        }
+        wsum = ws;
+        rhomax = rm;
+        err = e;
+    }
+};
+
+/* ------------------------------------------------------------ views */
+
+/* Build the CPU and (if any) memory chain views of task i at scale q.
+ * Gap definitions: analysis.py:89 cpu_inter_arrival, analysis.py:57
+ * mem_inter_arrival; GR lo from gpu.py:25 gpu_response_bounds. */
+template <class V>
+RT_HD void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
+    typedef Num<V> N;
+    const TaskRec &t = c.tr[i];
+    const i64 *sg = c.blob + t.seg;
+    const int m = t.m, p = t.p, g = m - 1;
+    const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
+    const i64 *gw_lo = ml_hi + p;
+    typename Num<V>::Qt perlo = t.isgpu ? q / (2 * (typename Num<V>::Qt)t.g) : q;
+    /* CPU chain */
+    {
+        VOff o(c.MC);
+        V *v = c.vc + (size_t)i * c.L.SC;
+        V P = 0, EP = 0;
+        for (int j = 0; j < m; j++) {
+            V e = N::sc(cl_hi[j], q);
+            v[o.e + j] = e;
+            v[o.P + j] = P;
+            v[o.EP + j] = EP;
+            EP += e;
+            if (j < m - 1) {
+                V gap;
+                if (c.mm == RTGPU_TWO_COPY)
+                    gap = N::sc(ml_lo[2 * j] + ml_lo[2 * j + 1], q) + (V)gw_lo[j] * (V)perlo;
+                else
+                    gap = N::sc(ml_lo[j], q) + (V)gw_lo[j] * (V)perlo;
+                P += e + gap;
+            }
+        }
+        V elast = v[o.e + m - 1];
+        v[o.EP + m] = EP;
+        v[o.F1] = P + elast + N::sc(t.T - t.D, q);
+        V wrap = N::sc(t.T - t.sClu - t.sMll, q) - (t.isgpu ? (V)t.sGWlo * (V)perlo : (V)0);
+        v[o.WN] = wrap < 0 ? (V)1 : (V)0;
+        v[o.P + m] = P + elast + (wrap < 0 ? (V)0 : wrap);
+        (void)g;
+    }
+    /* memory chain */
+    if (p > 0) {
+        VOff o(c.MP);
+        V *v = c.vm + (size_t)i * c.L.SM;
+        V P = 0, EP = 0;
+        for (int j = 0; j < p; j++) {
+            V e = N::sc(ml_hi[j], q);
+            v[o.e + j] = e;
+            v[o.P + j] = P;
+            v[o.EP + j] = EP;
+            EP += e;
+            if (j < p - 1) {
+                V gap;
+                if (c.mm == RTGPU_TWO_COPY)
+                    gap = (j % 2 == 0) ? (V)gw_lo[j / 2] * (V)perlo : N::sc(cl_lo[(j + 1) / 2], q);
+                else
+                    gap = (V)gw_lo[j] * (V)perlo + N::sc(cl_lo[j + 1], q);
+                P += e + gap;
+            }
+        }
+        V elast = v[o.e + p - 1];
+        v[o.EP + p] = EP;
+        V first = N::sc(t.T - t.D + cl_lo[m - 1] + cl_lo[0], q);
+        if (c.mm == RTGPU_ONE_COPY) first += (V)gw_lo[m - 2] * (V)perlo;
+        v[o.F1] = P + elast + first;
+        V wrap = N::sc(t.T - t.sMlu - t.innerCll, q) - (V)t.sGWlo * (V)perlo;
+        v[o.WN] = wrap < 0 ? (V)1 : (V)0;
+        v[o.P + p] = P + elast + (wrap < 0 ? (V)0 : wrap);
+    }
+}
+
+/* Views of tasks [0, k) at scale q (reused when already current). */
+template <class V, class TM>
+RT_HD void ensure_views(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt q) {
+    if (c.vq == q && c.vn >= k) return;
+    int from = (c.vq == q) ? c.vn : 0;
+    tm.pfor(k - from, [&](int x) { build_view(c, from + x, q); });
+    c.vq = q;
+    c.vn = k;
+}
+
+/* ------------------------------------------------------------ chain walk */
+
+/* W_i^h(H) of suspension.py:77 chain_workload over the view, in O(p).
+ * rho = remaining slope-1 length (the walk ends inside a segment), err =
+ * an InfeasibleGapError the reference would raise (walk reaches the first
+ * negative wrap-around gap). */
+template <class V>
+RT_HD V walk(const V *v, int PM, int p, int h, V H, V &rho, bool &err) {
+    VOff o(PM);
+    rho = 0;
+    if (H <= 0) return 0;
+    const V *e = v + o.e, *P = v + o.P, *EP = v + o.EP;
+    V base = P[h];
+    V lim = H + base;
+    V F1 = v[o.F1];
+    if (F1 > lim) {
+        /* stops inside the first (partial) job: first x in [h, p-1] with
+         * P1[x+1] > lim, where P1[x+1] = P[x+1] for x < p-1 */
+        int x = h;
+        for (int y = h + 1; y < p; y++) x += (P[y] <= lim) ? 1 : 0;
+        V tail = lim - P[x];
+        V ex = e[x];
+        if (ex > tail) {
+            rho = ex - tail;
+            return EP[x] - EP[h] + tail;
+        }
+        return EP[x] - EP[h] + ex;
+    }
+    V w = EP[p] - EP[h];
+    V H2 = lim - F1; /* H minus the first job's span */
+    if (v[o.WN] != 0) {
+        /* negative wrap: the walk raises iff it reaches index 2p-1 */
+        if (P[p - 1] <= H2) {
+            err = true;
+            return 0;
+        }
+        int x = 0;
+        for (int y = 1; y < p - 1; y++) x += (P[y] <= H2) ? 1 : 0;
+        V tail = H2 - P[x];
+        if (e[x] > tail) {
+            rho = e[x] - tail;
+            return w + EP[x] + tail;
+        }
+        return w + EP[x] + e[x];
+    }
+    V C = P[p];
+    if (C <= 0) {
+        /* all-zero period: the reference loops forever */
+        err = true;
+        return 0;
+    }
+    V k = Num<V>::floordiv(H2, C);
+    V H3 = H2 - k * C;
+    w += k * EP[p];
+    int x = 0;
+    for (int y = 1; y < p; y++) x += (P[y] <= H3) ? 1 : 0;
+    V tail = H3 - P[x];
+    if (e[x] > tail) {
+        rho = e[x] - tail;
+        return w + EP[x] + tail;
+    }
+    return w + EP[x] + e[x];
+}
+
+/* Sum over hp(k) of max over start segments of W (analysis.py:131
+ * _max_workload summed as in mem_response / cpu_response). */
+template <class V, class TM>
+RT_HD V interference(const TM &tm, SetCtx<V> &c, int k, int kind, V H, V &rho, bool &err) {
+    rho = 0;
+    err = false;
+    if (H <= 0 || k == 0) return 0;
+    const int G = kind == K_CPU ? c.GC : c.GM;
+    const int tpr = 32 / G;
+    const int PM = kind == K_CPU ? c.MC : c.MP;
+    const int stride = kind == K_CPU ? c.L.SC : c.L.SM;
+    const V *views = kind == K_CPU ? c.vc : c.vm;
+    const i64 prio_k = c.tr[k].prio;
+    V total = 0;
+    for (int i0 = 0; i0 < k; i0 += tpr) {
+        V ws, rm;
+        bool e;
+        tm.group_reduce(G, [&](int slot, V &w, V &r, bool &es) {
+            int i = i0 + slot / G, h = slot % G;
+            if (i < k) {
+                const TaskRec &ti = c.tr[i];
+                int p = kind == K_CPU ? ti.m : ti.p;
+                if (h < p && ti.prio < prio_k)
+                    w = walk(views + (size_t)i * stride, PM, p, h, H, r, es);
+            }
+        }, ws, rm, e);
+        total += ws;
+        if (rm > rho) rho = rm;
+        if (e) err = true;
+    }
+    return total;
+}
+
+/* Least fixed point of r = base + I(r) searched from `start` (base <= start
+ * <= lfp).  Returns -1 for the reference's None (suspension.py:123: iterate
+ * beyond the bound, or an InfeasibleGapError inside the interference). */
+template <class V, class TM>
+RT_HD V lfp(const TM &tm, SetCtx<V> &c, int k, int kind, V base, V start, V bound) {
+    if (base > bound) return (V)-1;
+    V r = start;
+    for (int it = 0; it < ITER_CAP; it++) {
+        V rho;
+        bool err;
+        V I = interference(tm, c, k, kind, r, rho, err);
+        if (err) return (V)-1;
+        V nxt = base + I;
+        if (nxt <= r) return r; /* nxt == r in exact arithmetic */
+        nxt += rho; /* slope-1 jump: nxt + rho <= lfp, so exceeding the
+                     * bound here means lfp > bound (reference: None) */
+        if (nxt > bound) return (V)-1;
+        r = nxt;
+    }
+    c.stuck = 1;
+    return (V)-1;
+}
+
+/* Fixed points for several bases sharing one interference function, with
+ * warm starts: lfp(b') >= lfp(b) + (b' - b) for b' >= b, and None(b) implies
+ * None(b') (both monotone).  Results in out[] (-1 = None). */
+template <class V, class TM>
+RT_HD void lfp_many(const TM &tm, SetCtx<V> &c, int k, int kind, const V *bases, V *out, int cnt,
+                    V bound, bool stop_on_none, bool &any_none) {
+    any_none = false;
+    for (int j = 0; j < cnt; j++) {
+        V b = bases[j], start = b;
+        bool none = false;
+        for (int q = 0; q < j; q++) {
+            if (bases[q] <= b) {
+                if (out[q] < 0) none = true;
+                else start = tmax(start, out[q] + (b - bases[q]));
+            }
+        }
+        V r = none ? (V)-1 : lfp(tm, c, k, kind, b, start, bound);
+        tm.sync();
+        if (tm.leader()) out[j] = r;
+        tm.sync();
+        if (r < 0) {
+            any_none = true;
+            if (stop_on_none) {
+                for (int q = j + 1; q < cnt; q++)
+                    if (tm.leader()) out[q] = (V)-1;
+                tm.sync();
+                return;
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------ task evaluation */
+
+template <class V> struct TaskEval {
+    /* results at scale q (numerators), -1 = None */
+    typename Num<V>::Qt q;
+    V e2e, r1, r2;
+    bool pass;
+};
+
+/* Scale for evaluating task k at count g given the prefix lcm. */
+template <class V>
+RT_HD typename Num<V>::Qt task_scale(SetCtx<V> &c, int k, int g, typename Num<V>::Qt lcm_pre) {
+    typedef typename Num<V>::Qt Qt;
+    Qt q = lcm_lim<Qt>(lcm_pre, (Qt)1, c.qlim);
+    q = (q == 0 || q > c.qlim / 2) ? 0 : q * 2;
+    if (q != 0 && c.tr[k].isgpu) q = lcm_lim<Qt>(q, (Qt)2 * (Qt)c.A * (Qt)g, c.qlim);
+    if (q == 0) c.esc = 1;
+    return q;
+}
+
+/* GR^j up (gpu.py:25) summed over task k's kernels, at scale q:
+ * sum_j[(gw_hi*an - gl*A)/(2*A*g) + gl] = sInfl*(q/(2Ag)) + sGL*q. */
+template <class V>
+RT_HD V sum_grup(const SetCtx<V> &c, int k, int g, typename Num<V>::Qt q) {
+    const TaskRec &t = c.tr[k];
+    if (!t.isgpu) return 0;
+    typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * g);
+    return (V)t.sInfl * (V)per + Num<V>::sc(t.sGL, q);
+}
+
+/*
+ * Full evaluation of task k at count g (prefix fixed), exactly as
+ * analysis.py:284-296 (mem_response for every memory segment, cpu_response
+ * for every CPU segment, end_to_end).  want_all: compute every value (report
+ * pass); otherwise stop as soon as the verdict is known.  mr_out/cr_out (may
+ * be null) receive per-segment numerators at scale q.
+ */
+template <class V, class TM>
+RT_HD void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::Qt lcm_pre,
+                     bool want_all, TaskEval<V> &res, V *mr_out, V *cr_out) {
+    typedef Num<V> N;
+    const TaskRec &t = c.tr[k];
+    typename N::Qt q = task_scale(c, k, g, lcm_pre);
+    res.q = q;
+    res.pass = false;
+    res.e2e = res.r1 = res.r2 = (V)-1;
+    if (c.esc) return;
+    c.evals++;
+    ensure_views(tm, c, k, q);
+    const V D = N::sc(t.D, q);
+    V *bases = c.scr;
+    V *outs = c.scr + (c.MP + c.MC + 2);
+    const i64 *sg = c.blob + t.seg;
+    const i64 *cl_hi = sg + t.m, *ml_hi = sg + 2 * t.m + t.p;
+    /* memory segments: analysis.py:156 (blocking = longest lp copy) */
+    V sum_mr = 0;
+    bool mr_none = false;
+    if (t.p > 0) {
+        tm.pfor(t.p, [&](int j) { bases[j] = N::sc(ml_hi[j] + t.B, q); });
+        lfp_many(tm, c, k, K_MEM, bases, outs, t.p, D, !want_all, mr_none);
+        for (int j = 0; j < t.p; j++)
+            if (outs[j] >= 0) sum_mr += outs[j];
+        if (mr_out) tm.pfor(t.p, [&](int j) { mr_out[j] = outs[j]; });
+        tm.sync();
+        if (mr_none && !want_all) return;
+    }
+    const V grup = sum_grup(c, k, g, q);
+    /* end_to_end R2 (analysis.py:214) first: it needs no per-segment CPU bounds */
+    V r2 = (V)-1;
+    if (!mr_none) r2 = lfp(tm, c, k, K_CPU, grup + sum_mr + N::sc(t.sClu, q),
+                           grup + sum_mr + N::sc(t.sClu, q), D);
+    res.r2 = r2;
+    if (r2 >= 0 && !want_all) {
+        res.pass = true;
+        res.e2e = r2;
+        return;
+    }
+    /* cpu_response for every CPU segment (analysis.py:175), then R1 */
+    tm.pfor(t.m, [&](int j) { bases[j] = N::sc(cl_hi[j], q); });
+    bool cr_none;
+    lfp_many(tm, c, k, K_CPU, bases, outs, t.m, D, !want_all, cr_none);
+    V sum_cr = 0;
+    for (int j = 0; j < t.m; j++)
+        if (outs[j] >= 0) sum_cr += outs[j];
+    if (cr_out) tm.pfor(t.m, [&](int j) { cr_out[j] = outs[j]; });
+    tm.sync();
+    V r1 = (V)-1;
+    if (!mr_none && !cr_none) {
+        V cand = grup + sum_mr + sum_cr;
+        if (cand <= D) r1 = cand;
+    }
+    res.r1 = r1;
+    if (mr_none) return;
+    if (r1 < 0) res.e2e = r2;
+    else if (r2 < 0) res.e2e = r1;
+    else res.e2e = tmin(r1, r2);
+    res.pass = res.e2e >= 0;
+}
+
+/* ------------------------------------------------------------ set loading */
+
+/* Per-task sums and flags (lane-parallel).  Computes the isolated-bound
+ * minimum count of analysis.py:239 _min_feasible_gn in closed form:
+ * sum_j[(gw_hi*a - gl*A)/(2*A*gn) + gl] + sum ml_hi + sum cl_hi <= D. */
+template <class V>
+RT_HD void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
+    const i64 *r = c.blob + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
+    TaskRec &t = c.tr[i];
+    t.m = (int)r[0];
+    t.p = (int)r[1];
+    t.D = r[2];
+    t.T = r[3];
+    t.prio = r[4];
+    t.seg = r[5];
+    t.idx = i;
+    t.flags = 0;
+    t.g = 0;
+    t.gmin = 0;
+    t.isgpu = t.m > 1;
+    const int m = t.m, p = t.p;
+    int want_p = m < 2 ? 0 : (c.mm == RTGPU_TWO_COPY ? 2 * m - 2 : m - 1);
+    if (m < 1 || m > c.MC || p != want_p || p > c.MP || t.T <= 0 || t.D <= 0 || t.D > t.T) {
+        t.flags |= TF_UNSUP;
+        *vb_out = 0;
+        return;
+    }
+    const i64 *sg = c.blob + t.seg;
+    const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
+    const int g = m - 1;
+    const i64 *gw_lo = ml_hi + p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+    i128 tot = 0;
+    t.sClu = t.sCll = t.sMlu = t.sMll = t.sGWlo = t.sInfl = t.sGL = t.innerCll = t.maxMlu = 0;
+    bool neg = false;
+    for (int j = 0; j < m; j++) {
+        t.sClu += cl_hi[j];
+        t.sCll += cl_lo[j];
+        neg = neg || cl_hi[j] < 0 || cl_lo[j] < 0;
+        if (j >= 1 && j <= m - 2) t.innerCll += cl_lo[j];
+    }
+    for (int j = 0; j < p; j++) {
+        t.sMlu += ml_hi[j];
+        t.sMll += ml_lo[j];
+        t.maxMlu = tmax(t.maxMlu, ml_hi[j]);
+        neg = neg || ml_hi[j] < 0 || ml_lo[j] < 0;
+    }
+    i128 infl_hi = 0;
+    for (int j = 0; j < g; j++) {
+        neg = neg || gw_lo[j] < 0 || gw_hi[j] < 0 || gl[j] < 0 || an[j] < 0;
+        i128 w = (i128)gw_hi[j] * an[j], o = (i128)gl[j] * c.A;
+        if (o > w) t.flags |= TF_INV;
+        t.sInfl += (i64)(w - o);
+        t.sGL += gl[j];
+        t.sGWlo += gw_lo[j];
+        infl_hi += w;
+    }
+    if (neg) {
+        t.flags |= TF_UNSUP;
+        *vb_out = 0;
+        return;
+    }
+    tot = (i128)t.sClu + t.sCll + t.sMlu + t.sMll + t.sGWlo + t.sGL + infl_hi / c.A + 1;
+    *vb_out = (i128)t.D + t.T + tot;
+    if (t.isgpu) {
+        /* infl/(2*A*gn) + fixed <= D  <=>  infl <= 2*A*gn*(D - fixed) */
+        i128 X = (i128)t.D - t.sGL - t.sMlu - t.sClu;
+        i128 gm = 0;
+        if (c.GN >= 1) {
+            if (X > 0) {
+                i128 den = 2 * (i128)c.A * X;
+                gm = ((i128)t.sInfl + den - 1) / den;
+                if (gm < 1) gm = 1;
+                if (gm > c.GN) gm = 0;
+            } else if (X == 0 && t.sInfl == 0) {
+                gm = 1;
+            }
+        }
+        if (gm == 0) t.flags |= TF_ISOFAIL;
+        t.gmin = (int)gm;
+        if (gm > 0) {
+            /* regular iff no wrap-around gap can be negative for any count >= gmin */
+            i128 twog = 2 * gm;
+            if (((i128)t.T - t.sClu - t.sMll) * twog - t.sGWlo < 0) t.flags |= TF_IRREG;
+            if (((i128)t.T - t.sMlu - t.innerCll) * twog - t.sGWlo < 0) t.flags |= TF_IRREG;
+        }
+    } else {
+        if (t.sClu > t.D) t.flags |= TF_ISOFAIL;
+        if (t.T - t.sClu < 0) t.flags |= TF_IRREG;
+    }
+}
+
+/* ------------------------------------------------------------ output helpers */
+
+template <class V> struct OutPtrs {
+    int32_t *vsm;   /* [n] */
+    i64 *e2e, *den; /* [n] */
+    i64 *detail;    /* set-blob shaped, or null */
+};
+
+/* Report pass over a fixed allocation (tr[].g) with per-task scales,
+ * exactly analysis.py:280-298 evaluate(): every memory / CPU segment bound,
+ * the GPU bounds of the allocation and the end-to-end bound; stops after the
+ * first failing task when stop_at_fail (the reference's per_task then holds
+ * the tasks up to it).  Values are written as numerators over den[k]. */
+template <class V, class TM>
+RT_HD bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool stop_at_fail) {
+    typedef typename Num<V>::Qt Qt;
+    Qt lcm_pre = 1;
+    V *mr = c.scr + 2 * (c.MP + c.MC + 2);
+    V *cr = mr + c.MP;
+    V *grl = cr + c.MC;
+    V *grh = grl + c.MC;
+    bool failed = false;
+    int k = 0;
+    for (; k < c.n; k++) {
+        const TaskRec &t = c.tr[k];
+        TaskEval<V> res;
+        eval_task(tm, c, k, t.g, lcm_pre, true, res, mr, cr);
+        if (c.esc || c.stuck) return false;
+        const Qt q = res.q;
+        const i64 *sg = c.blob + t.seg;
+        const int m = t.m, p = t.p, g = m - 1;
+        const i64 *gw_lo = sg + 2 * m + 2 * p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+        if (t.isgpu) {
+            const Qt perlo = q / (2 * (Qt)t.g);
+            const Qt perhi = q / (2 * (Qt)c.A * (Qt)t.g);
+            tm.pfor(g, [&](int j) {
+                grl[j] = (V)gw_lo[j] * (V)perlo;
+                V infl = (V)((i128)gw_hi[j] * an[j] - (i128)gl[j] * c.A);
+                grh[j] = infl * (V)perhi + Num<V>::sc(gl[j], q);
+            });
+        }
+        /* reduce by a common gcd so numerators and den fit int64 (only the
+         * 128-bit arithmetic can exceed it) */
+        i128 red = 1;
+        if (sizeof(V) > 8) {
+            i128 gg = (i128)q;
+            if (res.e2e >= 0) gg = gcdq<i128>(gg, Num<V>::wide(res.e2e));
+            for (int j = 0; j < p; j++)
+                if (mr[j] >= 0) gg = gcdq<i128>(gg, Num<V>::wide(mr[j]));
+            for (int j = 0; j < m; j++)
+                if (cr[j] >= 0) gg = gcdq<i128>(gg, Num<V>::wide(cr[j]));
+            for (int j = 0; j < g; j++) {
+                gg = gcdq<i128>(gg, Num<V>::wide(grl[j]));
+                gg = gcdq<i128>(gg, Num<V>::wide(grh[j]));
+            }
+            red = gg == 0 ? 1 : gg;
+            const i128 lim = (i128)INT64_MAX;
+            bool over = (i128)q / red > lim || (res.e2e >= 0 && Num<V>::wide(res.e2e) / red > lim);
+            for (int j = 0; j < g; j++) over = over || Num<V>::wide(grh[j]) / red > lim;
+            for (int j = 0; j < p; j++) over = over || (mr[j] >= 0 && Num<V>::wide(mr[j]) / red > lim);
+            for (int j = 0; j < m; j++) over = over || (cr[j] >= 0 && Num<V>::wide(cr[j]) / red > lim);
+            if (over) {
+                c.esc = 1; /* not representable even reduced */
+                return false;
+            }
+        }
+        auto num = [&](V v) -> i64 { return v < 0 ? (i64)RTGPU_NONE : (i64)(Num<V>::wide(v) / red); };
+        tm.sync();
+        if (tm.leader()) {
+            o.e2e[k] = num(res.e2e);
+            o.den[k] = (i64)((i128)q / red);
+        }
+        if (o.detail) {
+            i64 *d = o.detail + t.seg;
+            tm.pfor(2 * m + 2 * p + 4 * g, [&](int w) {
+                i64 v = RTGPU_ABSENT;
+                if (w < m) v = num(cr[w]);
+                else if (w >= 2 * m && w < 2 * m + p) v = num(mr[w - 2 * m]);
+                else if (w >= 2 * m + 2 * p && w < 2 * m + 2 * p + g) v = num(grl[w - 2 * m - 2 * p]);
+                else if (w >= 2 * m + 2 * p + g && w < 2 * m + 2 * p + 2 * g) v = num(grh[w - 2 * m - 2 * p - g]);
+                d[w] = v;
+            });
+        }
+        if (t.isgpu) {
+            lcm_pre = lcm_lim<Qt>(lcm_pre, (Qt)t.g, c.qlim);
+            if (lcm_pre == 0) {
+                c.esc = 1;
+                return false;
+            }
+        }
+        if (!res.pass) {
+            failed = true;
+            if (stop_at_fail) {
+                k++;
+                break;
+            }
+        }
+    }
+    for (; k < c.n; k++) {
+        if (tm.leader()) {
+            o.e2e[k] = RTGPU_ABSENT;
+            o.den[k] = 1;
+        }
+        if (o.detail) {
+            const TaskRec &t = c.tr[k];
+            i64 *d = o.detail + t.seg;
+            tm.pfor(2 * t.m + 2 * t.p + 4 * (t.m - 1), [&](int w) { d[w] = RTGPU_ABSENT; });
+        }
+    }
+    tm.sync();
+    return !failed;
+}
+
+/* Set the count of task k (leader write) and drop views that used the old one. */
+template <class V, class TM>
+RT_HD void set_g(const TM &tm, SetCtx<V> &c, int k, int g) {
+    tm.sync();
+    if (tm.leader()) c.tr[k].g = g;
+    tm.sync();
+    if (c.vn > k) c.vn = k;
+}
+
+/* smallest passing count in [lo, hi] for task k (own-count monotone), or 0 */
+template <class V, class TM>
+RT_HD int find_g(const TM &tm, SetCtx<V> &c, int k, int lo, int hi, typename Num<V>::Qt lcm_pre) {
+    TaskEval<V> r;
+    eval_task(tm, c, k, lo, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
+    if (c.esc) return 0;
+    if (r.pass) return lo;
+    if (lo >= hi) return 0;
+    eval_task(tm, c, k, hi, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
+    if (c.esc || !r.pass) return 0;
+    while (hi - lo > 1) {
+        int mid = lo + (hi - lo) / 2;
+        eval_task(tm, c, k, mid, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
+        if (c.esc) return 0;
+        if (r.pass) hi = mid;
+        else lo = mid;
+    }
+    return hi;
+}
+
+/* Greedy descent (regular sets): equals the lexicographically first
+ * schedulable allocation of the reference grid search. */
+template <class V, class TM>
+RT_HD int search_greedy(const TM &tm, SetCtx<V> &c) {
+    typedef typename Num<V>::Qt Qt;
+    Qt lcm_pre = 1;
+    i64 used = 0, rest_min = 0;
+    for (int k = 0; k < c.n; k++)
+        if (c.tr[k].isgpu) rest_min += c.tr[k].gmin;
+    for (int k = 0; k < c.n; k++) {
+        TaskRec &t = c.tr[k];
+        if (!t.isgpu) {
+            TaskEval<V> r;
+            eval_task(tm, c, k, 0, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
+            if (c.esc) return ST_ESCALATE;
+            if (c.stuck) return RTGPU_UNDECIDED;
+            if (!r.pass) return RTGPU_UNSCHEDULABLE;
+            continue;
+        }
+        rest_min -= t.gmin;
+        i64 gmax = c.GN - used - rest_min;
+        if (gmax < t.gmin) return RTGPU_UNSCHEDULABLE;
+        int g = find_g(tm, c, k, t.gmin, (int)gmax, lcm_pre);
+        if (c.esc) return ST_ESCALATE;
+        if (c.stuck) return RTGPU_UNDECIDED;
+        if (g == 0) return RTGPU_UNSCHEDULABLE;
+        set_g(tm, c, k, g);
+        used += g;
+        lcm_pre = lcm_lim<Qt>(lcm_pre, (Qt)g, c.qlim);
+        if (lcm_pre == 0) return ST_ESCALATE;
+    }
+    return RTGPU_SCHEDULABLE;
+}
+
+/* Exact depth-first search with prefix pruning (irregular sets). */
+template <class V, class TM>
+RT_HD int search_dfs(const TM &tm, SetCtx<V> &c) {
+    typedef typename Num<V>::Qt Qt;
+    int d = 0;
+    for (;;) {
+        if (d == c.n) return RTGPU_SCHEDULABLE;
+        if (c.budget > 0 && c.evals >= c.budget) return RTGPU_UNDECIDED;
+        TaskRec &t = c.tr[d];
+        Qt lcm_pre = 1;
+        i64 used = 0, after = 0;
+        for (int i = 0; i < d; i++)
+            if (c.tr[i].isgpu) {
+                lcm_pre = lcm_lim<Qt>(lcm_pre, (Qt)c.tr[i].g, c.qlim);
+                if (lcm_pre == 0) return ST_ESCALATE;
+                used += c.tr[i].g;
+            }
+        for (int i = d + 1; i < c.n; i++)
+            if (c.tr[i].isgpu) after += c.tr[i].gmin;
+        bool ok;
+        if (!t.isgpu) {
+            TaskEval<V> r;
+            eval_task(tm, c, d, 0, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
+            ok = r.pass;
+        } else {
+            i64 gmax = c.GN - used - after;
+            int g = gmax >= t.gmin ? find_g(tm, c, d, t.gmin, (int)gmax, lcm_pre) : 0;
+            ok = g != 0;
+            if (ok) set_g(tm, c, d, g);
+        }
+        if (c.esc) return ST_ESCALATE;
+        if (c.stuck) return RTGPU_UNDECIDED;
+        if (ok) {
+            d++;
+            continue;
+        }
+        /* backtrack: the deepest earlier GPU task with room for one more SM
+         * (it still passes: own-count monotone) */
+        for (;;) {
+            d--;
+            if (d < 0) return RTGPU_UNSCHEDULABLE;
+            TaskRec &b = c.tr[d];
+            if (!b.isgpu) continue;
+            i64 u = 0, a = 0;
+            for (int i = 0; i < d; i++)
+                if (c.tr[i].isgpu) u += c.tr[i].g;
+            for (int i = d + 1; i < c.n; i++)
+                if (c.tr[i].isgpu) a += c.tr[i].gmin;
+            if (b.g < c.GN - u - a) {
+                set_g(tm, c, d, b.g + 1);
+                d++;
+                break;
+            }
+        }
+    }
+}
+
+/* Whole pipeline for one set; returns the status (or ST_ESCALATE). */
+template <class V, class TM>
+RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<V> &o) {
+    typedef typename Num<V>::Qt Qt;
+    const i64 *h = c.blob;
+    c.n = (int)h[0];
+    c.GN = (int)h[1];
+    c.mm = (int)h[2];
+    c.A = h[3];
+    c.vn = 0;
+    c.vq = 0;
+    c.esc = 0;
+    c.stuck = 0;
+    c.evals = 0;
+    c.budget_hit = 0;
+    tm.pfor(c.n, [&](int i) {
+        o.vsm[i] = 0;
+        o.e2e[i] = RTGPU_ABSENT;
+        o.den[i] = 1;
+    });
+    if (c.n < 0 || c.n > c.maxn || c.A < 1 || (c.mm != 0 && c.mm != 1)) return RTGPU_INVALID;
+    /* per-task loading; range bound = (n + 2M + 4) * max(D + T + sums) */
+    i128 vb_max = 0;
+    {
+        /* lanes load tasks; reduce the bound through the TaskRec B field */
+        tm.pfor(c.n, [&](int i) {
+            i128 vb;
+            load_task(c, i, &vb);
+            /* store the clamped bound temporarily in B (recomputed below) */
+            c.tr[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
+        });
+        for (int i = 0; i < c.n; i++) vb_max = tmax(vb_max, (i128)c.tr[i].B);
+    }
+    for (int k = 0; k < c.n; k++)
+        if (c.tr[k].flags & TF_UNSUP) return RTGPU_INVALID;
+    /* reference order: the first task whose min-SM search raises or fails */
+    for (int k = 0; k < c.n; k++) {
+        if (c.tr[k].flags & TF_INV) return RTGPU_INVALID;
+        if (c.tr[k].flags & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE;
+    }
+    i64 need = 0;
+    bool irregular = false;
+    for (int k = 0; k < c.n; k++) {
+        if (c.tr[k].isgpu) need += c.tr[k].gmin;
+        if (c.tr[k].flags & TF_IRREG) irregular = true;
+    }
+    if (need > c.GN) return RTGPU_UNSCHEDULABLE;
+    i128 factor = (i128)c.n + 2 * RTGPU_MAX_M + 4;
+    i128 vb = vb_max * factor;
+    if (vb > (i128)Num<V>::limit()) return ST_ESCALATE;
+    c.Vb = (i64)vb;
+    c.qlim = (Qt)(Num<V>::limit() / (Qt)c.Vb);
+    tm.sync();
+    /* mem blocking term of analysis.py:162: longest copy of any lower-priority task */
+    tm.pfor(c.n, [&](int k) {
+        i64 b = 0;
+        for (int i = 0; i < c.n; i++)
+            if (c.tr[i].prio > c.tr[k].prio) b = tmax(b, c.tr[i].maxMlu);
+        c.tr[k].B = b;
+    });
+    int st = irregular ? search_dfs(tm, c) : search_greedy(tm, c);
+    if (st == ST_ESCALATE) return st;
+    if (st == RTGPU_SCHEDULABLE) {
+        tm.pfor(c.n, [&](int i) { o.vsm[i] = c.tr[i].isgpu ? 2 * c.tr[i].g : 0; });
+    }
+    if ((flags & (RTGPU_F_BOUNDS | RTGPU_F_DETAIL)) &&
+        (st == RTGPU_SCHEDULABLE || st == RTGPU_UNSCHEDULABLE)) {
+        if (st == RTGPU_UNSCHEDULABLE) {
+            /* the reference reports the last allocation it tried: the
+             * lexicographically largest one (first GPU task takes the rest) */
+            int first = -1;
+            i64 others = 0;
+            for (int k = 0; k < c.n; k++)
+                if (c.tr[k].isgpu) {
+                    if (first < 0) first = k;
+                    else others += c.tr[k].gmin;
+                }
+            tm.sync();
+            if (tm.leader())
+                for (int k = 0; k < c.n; k++)
+                    c.tr[k].g = c.tr[k].isgpu ? (k == first ? (int)(c.GN - others) : c.tr[k].gmin) : 0;
+            tm.sync();
+            c.vn = 0;
+        }
+        c.stuck = 0;
+        report_pass(tm, c, o, st == RTGPU_UNSCHEDULABLE);
+        if (c.esc) return ST_ESCALATE;
+        if (c.stuck) return RTGPU_UNDECIDED;
+    }
+    return st;
+}
+
+}  // namespace rtgpu

@@ -1,0 +1,141 @@
+/*
+ * kernel.cuh -- the persistent warp-per-set kernel and its launcher,
+ * instantiated once per arithmetic in rtgpu_k_{f64,i64,i128}.cu (separate
+ * translation units so the three instantiations compile in parallel).
+ */
+#pragma once
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include "engine_core.cuh"
+
+namespace rtgpu {
+
+struct KParams {
+    const i64 *blobs, *set_off, *task_base;
+    i64 n_sets;
+    Dims dims;
+    int GC, GM;
+    unsigned flags;
+    i64 budget;
+    int32_t *status;
+    i64 *evals;
+    int32_t *vsm;
+    i64 *e2e, *den, *detail;
+    unsigned long long *ctr; /* [0..2] work counters, [3..4] escalation counts */
+    i64 *esc0, *esc1;        /* escalation lists (stage 0 -> 1, 1 -> 2) */
+};
+
+template <class V>
+__global__ void __launch_bounds__(256) analyze_kernel(KParams p, int stage) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    Layout<V> L;
+    L.init(p.dims);
+    unsigned char *slab = smem + (size_t)warp * L.bytes;
+    SetCtx<V> c;
+    c.tr = (TaskRec *)slab;
+    c.vc = (V *)(slab + L.off_views_c);
+    c.vm = (V *)(slab + L.off_views_m);
+    c.scr = (V *)(slab + L.off_scr);
+    c.L = L;
+    c.maxn = p.dims.maxn;
+    c.MC = p.dims.MC;
+    c.MP = p.dims.MP;
+    c.GC = p.GC;
+    c.GM = p.GM;
+    c.budget = p.budget;
+    WarpTeam tm{lane};
+    const i64 count = stage == 0 ? p.n_sets : (i64)(stage == 1 ? p.ctr[3] : p.ctr[4]);
+    const i64 *list = stage == 0 ? nullptr : (stage == 1 ? p.esc0 : p.esc1);
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(&p.ctr[stage], 1ull);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if ((i64)idx >= count) break;
+        const i64 s = list ? list[idx] : (i64)idx;
+        c.blob = p.blobs + p.set_off[s];
+        const i64 tb = p.task_base[s];
+        OutPtrs<V> o;
+        o.vsm = p.vsm + tb;
+        o.e2e = p.e2e + tb;
+        o.den = p.den + tb;
+        o.detail = p.detail ? p.detail + p.set_off[s] : nullptr;
+        int st = analyze_set(tm, c, p.flags, o);
+        if (st == ST_ESCALATE) {
+            if (stage < 2) {
+                if (lane == 0) {
+                    unsigned long long pos = atomicAdd(&p.ctr[3 + stage], 1ull);
+                    (stage == 0 ? p.esc0 : p.esc1)[pos] = s;
+                }
+                __syncwarp();
+                continue;
+            }
+            st = RTGPU_RANGE;
+        }
+        if (lane == 0) {
+            p.status[s] = st;
+            p.evals[s] = c.evals;
+        }
+        __syncwarp();
+    }
+}
+
+
+void set_err(const char *what, cudaError_t e);
+void set_err_msg(const char *msg);
+void count_launch();
+
+inline int pow2_group(int p) {
+    int g = 1;
+    while (g < p) g <<= 1;
+    return g < 1 ? 1 : (g > 32 ? 32 : g);
+}
+
+template <class V> inline int warps_per_block(const Dims &d, int *bytes_out) {
+    Layout<V> L;
+    L.init(d);
+    int wpb = 8;
+    while (wpb > 1 && (size_t)L.bytes * wpb > 200 * 1024) wpb >>= 1;
+    *bytes_out = L.bytes * wpb;
+    return (size_t)L.bytes * wpb > 220 * 1024 ? 0 : wpb;
+}
+
+template <class V> inline int launch_stage(const KParams &p, int stage, cudaStream_t st) {
+    int bytes = 0;
+    int wpb = warps_per_block<V>(p.dims, &bytes);
+    if (wpb == 0) {
+        set_err_msg("task sets too large for shared memory");
+        return -3;
+    }
+    cudaError_t e = cudaFuncSetAttribute(analyze_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) {
+        set_err("cudaFuncSetAttribute", e);
+        return -4;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, analyze_kernel<V>, 32 * wpb, bytes);
+    if (per_sm < 1) per_sm = 1;
+    i64 need = stage == 0 ? (p.n_sets + wpb - 1) / wpb : (i64)sms * per_sm;
+    i64 grid = (i64)sms * per_sm;
+    if (stage == 0 && need < grid) grid = need;
+    if (grid < 1) grid = 1;
+    analyze_kernel<V><<<(unsigned)grid, 32 * wpb, bytes, st>>>(p, stage);
+    count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_err("analyze_kernel launch", e);
+        return -5;
+    }
+    return 0;
+}
+
+
+int launch_stage_f64(const KParams &p, int stage, cudaStream_t st);
+int launch_stage_i64(const KParams &p, int stage, cudaStream_t st);
+int launch_stage_i128(const KParams &p, int stage, cudaStream_t st);
+
+}  // namespace rtgpu

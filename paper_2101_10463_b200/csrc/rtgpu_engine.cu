@@ -1,0 +1,209 @@
+/*
+ * rtgpu_engine.cu -- sm_100a kernels and the C-ABI of include/rtgpu.h.
+ *
+ * One warp analyses one task set (engine_core.cuh).  Warps are persistent:
+ * each pulls the next set index from a global counter, so the very uneven
+ * per-set cost (an isolated-bound rejection costs ~nothing, a schedulable
+ * 16-task set hundreds of fixed points) load-balances across the 148 SMs.
+ *
+ * Three stages run back to back on one stream with no host round trip:
+ *   stage 0  V = double  (integer-valued FP64, exact below 2^52)  all sets
+ *   stage 1  V = int64   (exact below 2^62)   sets stage 0 escalated
+ *   stage 2  V = int128  (exact below 2^125)  sets stage 1 escalated
+ * A stage appends the sets whose exact scaled range it cannot hold to the
+ * next stage's list; the next stage reads the count from device memory.
+ */
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/rtgpu.h"
+#include "kernel.cuh"
+
+using namespace rtgpu;
+
+namespace rtgpu {
+char g_err[512] = "";
+i64 g_launches = 0;
+void set_err(const char *what, cudaError_t e) {
+    snprintf(g_err, sizeof g_err, "%s: %s", what, e == cudaSuccess ? "error" : cudaGetErrorString(e));
+}
+void set_err_msg(const char *msg) { snprintf(g_err, sizeof g_err, "%s", msg); }
+void count_launch() { g_launches++; }
+}  // namespace rtgpu
+
+namespace {
+
+/* ------------------------------------------------------------ library state */
+
+std::mutex g_mu;
+
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t n = 0;
+    bool ensure(size_t bytes) {
+        if (bytes <= n) return true;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return false;
+        n = bytes;
+        return true;
+    }
+};
+
+DevBuf g_scratch; /* counters + escalation lists */
+DevBuf g_h_blobs, g_h_off, g_h_tb, g_h_status, g_h_evals, g_h_vsm, g_h_e2e, g_h_den, g_h_detail;
+
+int scan_dims_host(const i64 *blobs, const i64 *set_off, i64 n_sets, Dims *d) {
+    d->maxn = 1;
+    d->MC = 1;
+    d->MP = 0;
+    for (i64 s = 0; s < n_sets; s++) {
+        const i64 *h = blobs + set_off[s];
+        if (h[0] > d->maxn) d->maxn = (int)h[0];
+        if (h[5] > d->MC) d->MC = (int)h[5];
+        if (h[6] > d->MP) d->MP = (int)h[6];
+    }
+    if (d->maxn > RTGPU_MAX_TASKS) d->maxn = RTGPU_MAX_TASKS;
+    if (d->MC > RTGPU_MAX_M) d->MC = RTGPU_MAX_M;
+    if (d->MP > 2 * RTGPU_MAX_M - 2) d->MP = 2 * RTGPU_MAX_M - 2;
+    return 0;
+}
+
+int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base, i64 n_sets,
+               const Dims &dims, int method, unsigned flags, i64 budget, int32_t *d_status,
+               i64 *d_evals, int32_t *d_vsm, i64 *d_e2e, i64 *d_den, i64 *d_detail,
+               cudaStream_t st) {
+    if (method != RTGPU_METHOD_RTGPU) {
+        snprintf(g_err, sizeof g_err, "method %d not implemented by the engine", method);
+        return -2;
+    }
+    g_launches = 0;
+    if (n_sets <= 0) return 0;
+    size_t need = 8 * sizeof(unsigned long long) + 2 * sizeof(i64) * (size_t)n_sets;
+    if (!g_scratch.ensure(need)) {
+        set_err("cudaMalloc scratch", cudaGetLastError());
+        return -6;
+    }
+    KParams p;
+    p.blobs = d_blobs;
+    p.set_off = d_set_off;
+    p.task_base = d_task_base;
+    p.n_sets = n_sets;
+    p.dims = dims;
+    p.GC = pow2_group(dims.MC);
+    p.GM = pow2_group(dims.MP > 0 ? dims.MP : 1);
+    p.flags = flags;
+    p.budget = budget > 0 ? budget : (i64)1 << 22;
+    p.status = d_status;
+    p.evals = d_evals;
+    p.vsm = d_vsm;
+    p.e2e = d_e2e;
+    p.den = d_den;
+    p.detail = d_detail;
+    p.ctr = (unsigned long long *)g_scratch.p;
+    p.esc0 = (i64 *)((char *)g_scratch.p + 8 * sizeof(unsigned long long));
+    p.esc1 = p.esc0 + n_sets;
+    cudaError_t e = cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) {
+        set_err("cudaMemsetAsync", e);
+        return -7;
+    }
+    int rc = launch_stage_f64(p, 0, st);
+    if (!rc) rc = launch_stage_i64(p, 1, st);
+    if (!rc) rc = launch_stage_i128(p, 2, st);
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rtgpu_abi_version(void) { return RTGPU_ABI_VERSION; }
+
+const char *rtgpu_last_error(void) { return g_err; }
+
+int64_t rtgpu_last_launch_count(void) { return g_launches; }
+
+int rtgpu_device_info(int *n_devices, int *sm_count, int *cc_major, int *cc_minor) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        set_err("cudaGetDeviceCount", e);
+        if (n_devices) *n_devices = 0;
+        return -1;
+    }
+    if (n_devices) *n_devices = n;
+    if (n > 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (sm_count) cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+        if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+        if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    }
+    return 0;
+}
+
+int rtgpu_analyze_device(const int64_t *d_blobs, const int64_t *d_set_off,
+                         const int64_t *d_task_base, int64_t n_sets, int max_tasks, int max_m,
+                         int max_p, int method, unsigned flags, int64_t eval_budget,
+                         int32_t *d_status, int64_t *d_evals, int32_t *d_vsm, int64_t *d_e2e_num,
+                         int64_t *d_den, int64_t *d_detail, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Dims d;
+    d.maxn = max_tasks < 1 ? 1 : max_tasks;
+    d.MC = max_m < 1 ? 1 : max_m;
+    d.MP = max_p < 0 ? 0 : max_p;
+    if (d.maxn > RTGPU_MAX_TASKS || d.MC > RTGPU_MAX_M || d.MP > 2 * RTGPU_MAX_M - 2) {
+        snprintf(g_err, sizeof g_err, "dims exceed engine limits");
+        return -1;
+    }
+    return run_device((const i64 *)d_blobs, (const i64 *)d_set_off, (const i64 *)d_task_base, n_sets,
+                      d, method, flags, eval_budget, d_status, (i64 *)d_evals, d_vsm,
+                      (i64 *)d_e2e_num, (i64 *)d_den, (i64 *)d_detail, (cudaStream_t)stream);
+}
+
+int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64_t *task_base,
+                       int64_t n_sets, int method, unsigned flags, int64_t eval_budget,
+                       int32_t *status, int64_t *evals, int32_t *vsm, int64_t *e2e_num,
+                       int64_t *den, int64_t *detail) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (n_sets <= 0) return 0;
+    Dims d;
+    scan_dims_host((const i64 *)blobs, (const i64 *)set_off, n_sets, &d);
+    const size_t W = (size_t)set_off[n_sets], T = (size_t)task_base[n_sets];
+    if (!g_h_blobs.ensure(W * 8) || !g_h_off.ensure((n_sets + 1) * 8) ||
+        !g_h_tb.ensure((n_sets + 1) * 8) || !g_h_status.ensure(n_sets * 4) ||
+        !g_h_evals.ensure(n_sets * 8) || !g_h_vsm.ensure(T * 4) || !g_h_e2e.ensure(T * 8) ||
+        !g_h_den.ensure(T * 8) || (detail && !g_h_detail.ensure(W * 8))) {
+        set_err("cudaMalloc", cudaGetLastError());
+        return -6;
+    }
+    cudaStream_t st = 0;
+    cudaMemcpyAsync(g_h_blobs.p, blobs, W * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(g_h_off.p, set_off, (n_sets + 1) * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(g_h_tb.p, task_base, (n_sets + 1) * 8, cudaMemcpyHostToDevice, st);
+    int rc = run_device((const i64 *)g_h_blobs.p, (const i64 *)g_h_off.p, (const i64 *)g_h_tb.p,
+                        n_sets, d, method, flags, eval_budget, (int32_t *)g_h_status.p,
+                        (i64 *)g_h_evals.p, (int32_t *)g_h_vsm.p, (i64 *)g_h_e2e.p,
+                        (i64 *)g_h_den.p, detail ? (i64 *)g_h_detail.p : nullptr, st);
+    if (rc) return rc;
+    cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(e2e_num, g_h_e2e.p, T * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(den, g_h_den.p, T * 8, cudaMemcpyDeviceToHost, st);
+    if (detail) cudaMemcpyAsync(detail, g_h_detail.p, W * 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        set_err("rtgpu_analyze_host", e);
+        return -8;
+    }
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,6 @@
+/* rtgpu_k_i64.cu -- stage kernel instantiated for V = i64 (see kernel.cuh). */
+#include "kernel.cuh"
+
+namespace rtgpu {
+int launch_stage_i64(const KParams &p, int stage, cudaStream_t st) { return launch_stage<i64>(p, stage, st); }
+}  // namespace rtgpu

@@ -1,0 +1,95 @@
+/*
+ * TEST HARNESS ONLY -- never loaded by the package.
+ *
+ * Runs engine_core.cuh (the exact code the sm_100a kernels run) with the
+ * sequential SeqTeam emulation of a warp, so the CPU-only test suite can
+ * check the engine's algorithm (greedy search, closed-form walks,
+ * accelerated fixed points, range escalation) against the oracle without a
+ * GPU.  The product path is the CUDA build in paper_2101_10463_b200/csrc.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../paper_2101_10463_b200/csrc/engine_core.cuh"
+
+using namespace rtgpu;
+
+namespace {
+
+template <class V>
+int run_one(const Dims &d, const i64 *blob, unsigned flags, i64 budget, OutPtrs<V> o, i64 *evals) {
+    Layout<V> L;
+    L.init(d);
+    std::vector<unsigned char> slab((size_t)L.bytes + 64);
+    unsigned char *base = (unsigned char *)(((uintptr_t)slab.data() + 15) & ~(uintptr_t)15);
+    SetCtx<V> c;
+    c.blob = blob;
+    c.tr = (TaskRec *)base;
+    c.vc = (V *)(base + L.off_views_c);
+    c.vm = (V *)(base + L.off_views_m);
+    c.scr = (V *)(base + L.off_scr);
+    c.L = L;
+    c.maxn = d.maxn;
+    c.MC = d.MC;
+    c.MP = d.MP;
+    int g = 1;
+    while (g < d.MC) g <<= 1;
+    c.GC = g;
+    g = 1;
+    while (g < (d.MP > 0 ? d.MP : 1)) g <<= 1;
+    c.GM = g;
+    c.budget = budget > 0 ? budget : (i64)1 << 22;
+    SeqTeam tm;
+    int st = analyze_set(tm, c, flags, o);
+    *evals = c.evals;
+    return st;
+}
+
+}  // namespace
+
+extern "C" int host_analyze_batch(const int64_t *blobs, const int64_t *set_off,
+                                  const int64_t *task_base, int64_t n_sets, unsigned flags,
+                                  int64_t budget, int first_stage, int32_t *status,
+                                  int64_t *evals, int32_t *vsm, int64_t *e2e, int64_t *den,
+                                  int64_t *detail, int32_t *stage_used) {
+    Dims d;
+    d.maxn = 1;
+    d.MC = 1;
+    d.MP = 0;
+    for (int64_t s = 0; s < n_sets; s++) {
+        const int64_t *h = blobs + set_off[s];
+        if (h[0] > d.maxn) d.maxn = (int)h[0];
+        if (h[5] > d.MC) d.MC = (int)h[5];
+        if (h[6] > d.MP) d.MP = (int)h[6];
+    }
+    for (int64_t s = 0; s < n_sets; s++) {
+        const i64 *blob = (const i64 *)blobs + set_off[s];
+        int64_t tb = task_base[s];
+        int st = ST_ESCALATE;
+        int stage = first_stage;
+        for (; stage < 3 && st == ST_ESCALATE; stage++) {
+            i64 ev = 0;
+            if (stage == 0) {
+                OutPtrs<double> o{vsm + tb, (i64 *)e2e + tb, (i64 *)den + tb,
+                                  detail ? (i64 *)detail + set_off[s] : nullptr};
+                st = run_one<double>(d, blob, flags, budget, o, &ev);
+            } else if (stage == 1) {
+                OutPtrs<i64> o{vsm + tb, (i64 *)e2e + tb, (i64 *)den + tb,
+                               detail ? (i64 *)detail + set_off[s] : nullptr};
+                st = run_one<i64>(d, blob, flags, budget, o, &ev);
+            } else {
+                OutPtrs<i128> o{vsm + tb, (i64 *)e2e + tb, (i64 *)den + tb,
+                                detail ? (i64 *)detail + set_off[s] : nullptr};
+                st = run_one<i128>(d, blob, flags, budget, o, &ev);
+            }
+            evals[s] = ev;
+        }
+        if (st == ST_ESCALATE) st = RTGPU_RANGE;
+        status[s] = st;
+        if (stage_used) stage_used[s] = stage - 1;
+    }
+    return 0;
+}

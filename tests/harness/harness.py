@@ -1,0 +1,59 @@
+"""TEST HARNESS ONLY: ctypes binding of engine_host.cpp (engine core on CPU)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+SRC = os.path.join(HERE, "engine_host.cpp")
+CORE = os.path.join(ROOT, "paper_2101_10463_b200", "csrc", "engine_core.cuh")
+LIB = os.path.join(HERE, "libenginehost.so")
+_lib = None
+
+
+def build():
+    newest = max(os.path.getmtime(SRC), os.path.getmtime(CORE))
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+        subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", LIB, SRC],
+                       check=True)
+    return LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(LIB)
+        p64 = ctypes.POINTER(ctypes.c_int64)
+        p32 = ctypes.POINTER(ctypes.c_int32)
+        _lib.host_analyze_batch.argtypes = [p64, p64, p64, ctypes.c_int64, ctypes.c_uint,
+                                            ctypes.c_int64, ctypes.c_int, p32, p64, p32, p64,
+                                            p64, p64, p32]
+    return _lib
+
+
+def _p(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t)) if a is not None else None
+
+
+def analyze_batch(blobs, set_off, task_base, flags=2, budget=0, first_stage=0, detail=True):
+    S = len(set_off) - 1
+    T = int(task_base[-1])
+    out = dict(status=np.zeros(S, np.int32), evals=np.zeros(S, np.int64),
+               vsm=np.zeros(T, np.int32), e2e_num=np.zeros(T, np.int64),
+               den=np.ones(T, np.int64),
+               detail=np.zeros(len(blobs), np.int64) if detail else None,
+               stage=np.zeros(S, np.int32))
+    blobs = np.ascontiguousarray(blobs, np.int64)
+    lib().host_analyze_batch(
+        _p(blobs, ctypes.c_int64), _p(np.ascontiguousarray(set_off, np.int64), ctypes.c_int64),
+        _p(np.ascontiguousarray(task_base, np.int64), ctypes.c_int64), S, flags, budget,
+        first_stage, _p(out["status"], ctypes.c_int32), _p(out["evals"], ctypes.c_int64),
+        _p(out["vsm"], ctypes.c_int32), _p(out["e2e_num"], ctypes.c_int64),
+        _p(out["den"], ctypes.c_int64), _p(out["detail"], ctypes.c_int64),
+        _p(out["stage"], ctypes.c_int32))
+    return out
