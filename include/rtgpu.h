@@ -96,6 +96,8 @@ extern "C" {
 /* flags */
 #define RTGPU_F_BOUNDS 1u  /* fill e2e_num/den for the reported allocation   */
 #define RTGPU_F_DETAIL 2u  /* also the per-segment report (implies BOUNDS)   */
+#define RTGPU_F_FIRST_I64 4u  /* testing: start at the int64 stage          */
+#define RTGPU_F_FIRST_I128 8u /* testing: start at the int128 stage         */
 
 /* limits of the engine (checked on entry; larger sets -> RTGPU_INVALID) */
 #define RTGPU_MAX_TASKS 64
@@ -133,6 +135,13 @@ int rtgpu_analyze_device(const int64_t *d_blobs, const int64_t *d_set_off,
 
 /* number of kernel launches the last rtgpu_analyze_* call enqueued */
 int64_t rtgpu_last_launch_count(void);
+
+/* Stage timing: when enabled, each rtgpu_analyze_* call records CUDA events
+ * around its three stage kernels on the launching stream;
+ * rtgpu_last_stage_ms (which synchronises on the last event) returns their
+ * durations in ms and the number of sets each stage processed. */
+void rtgpu_set_stage_timing(int enable);
+int rtgpu_last_stage_ms(float *ms3, int64_t *sets3);
 
 #ifdef __cplusplus
 }

@@ -35,8 +35,8 @@ class GenParamsC(ctypes.Structure):
 
 
 EXPORTS = ("rtgpu_abi_version", "rtgpu_last_error", "rtgpu_device_info", "rtgpu_analyze_host",
-           "rtgpu_analyze_device", "rtgpu_last_launch_count", "rtgpu_gen_blob_words",
-           "rtgpu_generate", "rtgpu_sha512")
+           "rtgpu_analyze_device", "rtgpu_last_launch_count", "rtgpu_set_stage_timing",
+           "rtgpu_last_stage_ms", "rtgpu_gen_blob_words", "rtgpu_generate", "rtgpu_sha512")
 
 
 def lib():
@@ -60,6 +60,8 @@ def lib():
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p]
     L.rtgpu_last_launch_count.restype = ctypes.c_int64
+    L.rtgpu_set_stage_timing.argtypes = [ctypes.c_int]
+    L.rtgpu_last_stage_ms.argtypes = [ctypes.POINTER(ctypes.c_float), _p64]
     L.rtgpu_gen_blob_words.argtypes = [ctypes.POINTER(GenParamsC)]
     L.rtgpu_gen_blob_words.restype = ctypes.c_int64
     L.rtgpu_generate.argtypes = [ctypes.POINTER(GenParamsC), ctypes.c_int64, _p64,
@@ -129,6 +131,19 @@ def analyze_device(d_blobs, d_set_off, d_task_base, n_sets: int, dims: Sequence[
 
 def last_launch_count() -> int:
     return int(lib().rtgpu_last_launch_count())
+
+
+def set_stage_timing(enable: bool) -> None:
+    lib().rtgpu_set_stage_timing(1 if enable else 0)
+
+
+def last_stage_ms():
+    """(ms per stage kernel, sets per stage) of the last call, or None."""
+    ms = (ctypes.c_float * 3)()
+    sets = np.zeros(3, np.int64)
+    if lib().rtgpu_last_stage_ms(ms, _ptr(sets, ctypes.c_int64)) != 0:
+        return None
+    return [float(x) for x in ms], [int(x) for x in sets]
 
 
 def gen_params_c(n_tasks, n_subtasks, cpu_range, gpu_range, mem_range, util, mem_model_code,

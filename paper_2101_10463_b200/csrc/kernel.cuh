@@ -62,7 +62,9 @@ __global__ void __launch_bounds__(256) analyze_kernel(KParams p, int stage) {
         o.e2e = p.e2e + tb;
         o.den = p.den + tb;
         o.detail = p.detail ? p.detail + p.set_off[s] : nullptr;
-        int st = analyze_set(tm, c, p.flags, o);
+        const bool force = (stage == 0 && (p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) ||
+                           (stage == 1 && (p.flags & RTGPU_F_FIRST_I128));
+        int st = force ? (int)ST_ESCALATE : analyze_set(tm, c, p.flags, o);
         if (st == ST_ESCALATE) {
             if (stage < 2) {
                 if (lane == 0) {

@@ -56,6 +56,12 @@ struct DevBuf {
 };
 
 DevBuf g_scratch; /* counters + escalation lists */
+int g_timing = 0;
+unsigned long long *g_last_ctr = nullptr;
+i64 g_last_n = 0;
+cudaEvent_t g_ev[4];
+bool g_ev_init = false;
+bool g_ev_valid = false;
 DevBuf g_h_blobs, g_h_off, g_h_tb, g_h_status, g_h_evals, g_h_vsm, g_h_e2e, g_h_den, g_h_detail;
 
 int scan_dims_host(const i64 *blobs, const i64 *set_off, i64 n_sets, Dims *d) {
@@ -113,9 +119,20 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
         set_err("cudaMemsetAsync", e);
         return -7;
     }
+    if (g_timing && !g_ev_init) {
+        for (int i = 0; i < 4; i++) cudaEventCreate(&g_ev[i]);
+        g_ev_init = true;
+    }
+    if (g_timing) cudaEventRecord(g_ev[0], st);
     int rc = launch_stage_f64(p, 0, st);
+    if (g_timing) cudaEventRecord(g_ev[1], st);
     if (!rc) rc = launch_stage_i64(p, 1, st);
+    if (g_timing) cudaEventRecord(g_ev[2], st);
     if (!rc) rc = launch_stage_i128(p, 2, st);
+    if (g_timing) cudaEventRecord(g_ev[3], st);
+    g_ev_valid = g_timing && !rc;
+    g_last_ctr = p.ctr;
+    g_last_n = n_sets;
     return rc;
 }
 
@@ -128,6 +145,29 @@ int rtgpu_abi_version(void) { return RTGPU_ABI_VERSION; }
 const char *rtgpu_last_error(void) { return g_err; }
 
 int64_t rtgpu_last_launch_count(void) { return g_launches; }
+
+void rtgpu_set_stage_timing(int enable) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_timing = enable;
+}
+
+int rtgpu_last_stage_ms(float *ms3, int64_t *sets3) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_ev_valid) return -1;
+    if (cudaEventSynchronize(g_ev[3]) != cudaSuccess) return -2;
+    for (int i = 0; i < 3; i++) {
+        ms3[i] = 0.f;
+        cudaEventElapsedTime(&ms3[i], g_ev[i], g_ev[i + 1]);
+    }
+    if (sets3) {
+        unsigned long long c[5] = {0, 0, 0, 0, 0};
+        cudaMemcpy(c, g_last_ctr, sizeof c, cudaMemcpyDeviceToHost);
+        sets3[0] = g_last_n;
+        sets3[1] = (int64_t)c[3];
+        sets3[2] = (int64_t)c[4];
+    }
+    return 0;
+}
 
 int rtgpu_device_info(int *n_devices, int *sm_count, int *cc_major, int *cc_minor) {
     int n = 0;

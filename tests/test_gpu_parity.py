@@ -1,0 +1,110 @@
+"""Parity of the CUDA engine (librtgpu.so on the B200) with the reference:
+golden reports produced by the reference itself, and the oracle on the
+reference generator's task sets.  Bit-exact: verdicts, allocations and every
+bound as an exact rational."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from golden_io import load_cases, ts_from_exact
+from oracle import oracle
+from paper_2101_10463_b200 import _native
+from paper_2101_10463_b200.analysis import analyze_batch, analyze_rtgpu
+from paper_2101_10463_b200.engine import DeviceBatch, analyze_packed
+from paper_2101_10463_b200.model import AnalysisMethod, report_to_dict
+from paper_2101_10463_b200.pack import (F_BOUNDS, F_DETAIL, INVALID, pack_tasksets,
+                                        unpack_report)
+
+pytestmark = pytest.mark.gpu
+
+F_FIRST_I64, F_FIRST_I128 = 4, 8
+
+
+@pytest.fixture(scope="module")
+def golden():
+    cases = load_cases()
+    return cases, pack_tasksets([ts_from_exact(c["taskset"]) for c in cases])
+
+
+def _check_golden(cases, batch, res):
+    bad = []
+    for s, c in enumerate(cases):
+        want = c["rtgpu"]
+        if "raises" in want:
+            if res.status[s] != INVALID:
+                bad.append(s)
+            continue
+        if report_to_dict(unpack_report(batch, res, s, AnalysisMethod.RTGPU)) != want:
+            bad.append(s)
+    return bad
+
+
+@pytest.mark.parametrize("first", [0, F_FIRST_I64, F_FIRST_I128])
+def test_gpu_matches_reference_reports(golden, first):
+    cases, batch = golden
+    res = analyze_packed(batch.blobs, batch.set_off, batch.task_base, 0, F_DETAIL | first)
+    assert not _check_golden(cases, batch, res)
+    assert _native.last_launch_count() == 3
+
+
+def test_dropin_api_matches_reference(golden):
+    cases, _ = golden
+    some = [c for c in cases if "raises" not in c["rtgpu"]][:60]
+    for c in some:
+        got = report_to_dict(analyze_rtgpu(ts_from_exact(c["taskset"])))
+        assert got == c["rtgpu"]
+    reps = analyze_batch([ts_from_exact(c["taskset"]) for c in some])
+    assert [report_to_dict(r) for r in reps] == [c["rtgpu"] for c in some]
+
+
+def _cmp(o, g_status, g_vsm, g_e2e, g_den):
+    assert np.array_equal(o["status"], g_status)
+    assert np.array_equal(o["vsm"], g_vsm)
+    for i in range(len(o["e2e_num"])):
+        a, b = int(o["e2e_num"][i]), int(g_e2e[i])
+        if a < 0 or b < 0:
+            assert a == b, i
+        else:
+            assert Fraction(a, int(o["den"][i])) == Fraction(b, int(g_den[i])), i
+
+
+@pytest.mark.parametrize("n,m,gn,u,mm,lo", [
+    (8, 5, 10, "1/5", 0, "1"), (8, 5, 10, "2/5", 0, "1"), (8, 5, 10, "3/5", 0, "1"),
+    (8, 5, 10, "4/5", 1, "7/10"), (5, 5, 10, "1/2", 1, "1"), (5, 3, 10, "1", 0, "3/5"),
+    (3, 3, 4, "1", 1, "1"), (6, 2, 20, "4/5", 0, "1"), (10, 4, 16, "1/2", 0, "1")])
+def test_gpu_matches_oracle_generated(n, m, gn, u, mm, lo):
+    gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), Fraction(u), mm,
+                              gn, Fraction(12, 100), Fraction(lo))
+    seeds = [f"9:{u}:{i}" for i in range(400)]
+    b, so, tb = _native.generate(gp, seeds)
+    o = oracle.analyze_batch(b, so, tb, flags=1, threads=8, detail=False, budget=3_000_000)
+    decided = o["status"] != 2
+    batch = DeviceBatch(b, so, tb)
+    out = batch.alloc_results()
+    batch.run(out, flags=F_BOUNDS)
+    g = out.to_host()
+    assert decided.mean() > 0.9
+    idx = np.nonzero(decided)[0]
+    tmask = np.repeat(decided, n)
+    _cmp({k: (v[idx] if k == "status" else v[tmask]) for k, v in o.items() if k != "detail"
+          and k != "evals"},
+         g.status[idx], g.vsm[tmask], g.e2e_num[tmask], g.den[tmask])
+
+
+def test_device_batch_all_stages_agree():
+    gp = _native.gen_params_c(8, 5, (1000, 20000), (1000, 20000), (250, 5000), Fraction(2, 5), 0,
+                              10, Fraction(12, 100), Fraction(1))
+    b, so, tb = _native.generate(gp, list(range(2000)))
+    batch = DeviceBatch(b, so, tb)
+    outs = []
+    for first in (0, F_FIRST_I64, F_FIRST_I128):
+        out = batch.alloc_results()
+        batch.run(out, flags=F_BOUNDS | first)
+        outs.append(out.to_host())
+    for r in outs[1:]:
+        assert np.array_equal(r.status, outs[0].status)
+        assert np.array_equal(r.vsm, outs[0].vsm)
+        f0 = [Fraction(int(a), int(d)) for a, d in zip(outs[0].e2e_num, outs[0].den) if a >= 0]
+        f1 = [Fraction(int(a), int(d)) for a, d in zip(r.e2e_num, r.den) if a >= 0]
+        assert f0 == f1
