@@ -12,7 +12,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librtgpu.so")
+LIB_PATH = os.environ.get("RTGPU_LIB") or os.path.join(HERE, "librtgpu.so")
 
 _p64 = ctypes.POINTER(ctypes.c_int64)
 _p32 = ctypes.POINTER(ctypes.c_int32)

@@ -38,26 +38,33 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    lib = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
     os.makedirs(OBJDIR, exist_ok=True)
     procs, objs = [], []
+    tag = "" if out is None else "." + os.path.basename(out)
     for src in SOURCES:  # one translation unit per arithmetic: compile in parallel
-        obj = os.path.join(OBJDIR, src + ".o")
+        obj = os.path.join(OBJDIR, src + tag + ".o")
         objs.append(obj)
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-c",
+               os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((cmd, subprocess.Popen(cmd, cwd=CSRC)))
     for cmd, pr in procs:
         if pr.wait() != 0:
             raise RuntimeError("build failed: " + " ".join(cmd))
-    link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
+    link = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs]
     subprocess.run(link, check=True, cwd=CSRC)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_2101_10463_b200.build [--force] [--out PATH -DNAME=VAL ...]
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else None
+    defs = [a[2:] for a in argv if a.startswith("-D")]
+    print(build(force="--force" in argv or out is not None, verbose=True, out=out, defines=defs))

@@ -41,8 +41,12 @@
 
 #ifdef __CUDACC__
 #define RT_HD __host__ __device__ inline
+/* out-of-line: one copy of each big routine keeps the kernel inside the
+ * instruction cache (the fully inlined kernel was ~680 KB of SASS) */
+#define RT_NI __host__ __device__ __noinline__
 #else
 #define RT_HD inline
+#define RT_NI inline
 #endif
 
 namespace rtgpu {
@@ -172,6 +176,7 @@ template <class V> struct SetCtx {
     int n, GN, mm;
     i64 A;
     int maxn, MC, MP, GC, GM; /* batch maxima, lane group sizes */
+    int lgC, lgM, halfC, halfM; /* log2 group sizes; binary-search first steps */
     i64 Vb;             /* range bound in input ticks */
     Qt qlim;            /* largest admissible scale: limit / Vb */
     /* current views: tasks [0, vn) at scale vq */
@@ -182,6 +187,21 @@ template <class V> struct SetCtx {
     i64 evals, budget;
     int budget_hit;
 };
+
+/* lane-group sizes (2^lg lanes per hp task) and binary-search first steps */
+template <class V> RT_HD void set_groups(SetCtx<V> &c) {
+    int g = 1, lg = 0;
+    while (g < c.MC) g <<= 1, lg++;
+    c.GC = g;
+    c.lgC = lg;
+    c.halfC = g >> 1;
+    g = 1;
+    lg = 0;
+    while (g < (c.MP > 0 ? c.MP : 1)) g <<= 1, lg++;
+    c.GM = g;
+    c.lgM = lg;
+    c.halfM = g >> 1;
+}
 
 /* ------------------------------------------------------------ teams */
 
@@ -207,28 +227,46 @@ struct WarpTeam {
         __syncwarp();
     }
     __device__ __forceinline__ bool any(bool b) const { return __any_sync(0xffffffffu, b); }
-    /* slot = lane; f(slot, w, rho, err).  Max (w, then rho) within groups of
-     * G lanes, then sum of w and max of rho across groups. */
+    /* Interference rounds: slot = lane; f(slot, w, rho, err) gives the walk
+     * of one (task, start segment) pair.  Per round only the max over the
+     * 2^lg lanes of a task is shuffled; each lane accumulates its group's
+     * max and, if it is a maximiser, its rho.  acc_finish sums the groups
+     * and takes the rho max once for all rounds. */
+    template <class V> struct Acc {
+        V sum, rho;
+        bool err;
+    };
+    template <class V> __device__ __forceinline__ void acc_init(Acc<V> &a) const {
+        a.sum = 0;
+        a.rho = 0;
+        a.err = false;
+    }
     template <class V, class F>
-    __device__ __forceinline__ void group_reduce(int G, F f, V &wsum, V &rhomax, bool &err) const {
+    __device__ __forceinline__ void group_max_round(int lg, F f, Acc<V> &a) const {
         V w = 0, rho = 0;
         bool e = false;
         f(lane, w, rho, e);
-        for (int off = 1; off < G; off <<= 1) {
-            V w2 = shfl_x(w, off), r2 = shfl_x(rho, off);
-            if (w2 > w || (w2 == w && r2 > rho)) {
-                w = w2;
-                rho = r2;
-            }
+        V m = w;
+        for (int off = 1; off < (1 << lg); off <<= 1) {
+            V o = shfl_x(m, off);
+            if (o > m) m = o;
         }
-        for (int off = G; off < 32; off <<= 1) {
-            w += shfl_x(w, off);
-            V r2 = shfl_x(rho, off);
-            if (r2 > rho) rho = r2;
+        a.sum += m;
+        if (w == m && rho > a.rho) a.rho = rho;
+        a.err = a.err || e;
+    }
+    template <class V>
+    __device__ __forceinline__ void acc_finish(int lg, Acc<V> &a, V &wsum, V &rhomax, bool &err) const {
+        V s = a.sum;
+        for (int off = 1 << lg; off < 32; off <<= 1) s += shfl_x(s, off);
+        V r = a.rho;
+        for (int off = 1; off < 32; off <<= 1) {
+            V o = shfl_x(r, off);
+            if (o > r) r = o;
         }
-        wsum = w;
-        rhomax = rho;
-        err = __any_sync(0xffffffffu, e);
+        wsum = s;
+        rhomax = r;
+        err = __any_sync(0xffffffffu, a.err);
     }
 };
 #endif
@@ -241,27 +279,37 @@ struct SeqTeam {
         for (int i = 0; i < n; i++) f(i);
     }
     RT_HD bool any(bool b) const { return b; }
-    template <class V, class F> RT_HD void group_reduce(int G, F f, V &wsum, V &rhomax, bool &err) const {
-        V ws = 0, rm = 0;
-        bool e = false;
+    template <class V> struct Acc {
+        V sum, rho;
+        bool err;
+    };
+    template <class V> RT_HD void acc_init(Acc<V> &a) const {
+        a.sum = 0;
+        a.rho = 0;
+        a.err = false;
+    }
+    template <class V, class F> RT_HD void group_max_round(int lg, F f, Acc<V> &a) const {
+        const int G = 1 << lg;
         for (int g0 = 0; g0 < 32; g0 += G) {
-            V bw = 0, br = 0;
+            V w[32], r[32];
+            V m = 0;
             for (int s = g0; s < g0 + G; s++) {
-                V w = 0, rho = 0;
                 bool es = false;
-                f(s, w, rho, es);
-                e = e || es;
-                if (s == g0 || w > bw || (w == bw && rho > br)) {
-                    bw = w;
-                    br = rho;
-                }
+                w[s - g0] = 0;
+                r[s - g0] = 0;
+                f(s, w[s - g0], r[s - g0], es);
+                a.err = a.err || es;
+                if (s == g0 || w[s - g0] > m) m = w[s - g0];
             }
-            ws += bw;
-            if (br > rm) rm = br;
+            a.sum += m;
+            for (int s = 0; s < G; s++)
+                if (w[s] == m && r[s] > a.rho) a.rho = r[s];
         }
-        wsum = ws;
-        rhomax = rm;
-        err = e;
+    }
+    template <class V> RT_HD void acc_finish(int, Acc<V> &a, V &wsum, V &rhomax, bool &err) const {
+        wsum = a.sum;
+        rhomax = a.rho;
+        err = a.err;
     }
 };
 
@@ -271,7 +319,7 @@ struct SeqTeam {
  * Gap definitions: analysis.py:89 cpu_inter_arrival, analysis.py:57
  * mem_inter_arrival; GR lo from gpu.py:25 gpu_response_bounds. */
 template <class V>
-RT_HD void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
+RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     typedef Num<V> N;
     const TaskRec &t = c.tr[i];
     const i64 *sg = c.blob + t.seg;
@@ -355,7 +403,7 @@ RT_HD void ensure_views(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt q
  * an InfeasibleGapError the reference would raise (walk reaches the first
  * negative wrap-around gap). */
 template <class V>
-RT_HD V walk(const V *v, int PM, int p, int h, V H, V &rho, bool &err) {
+RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err) {
     VOff o(PM);
     rho = 0;
     if (H <= 0) return 0;
@@ -364,10 +412,13 @@ RT_HD V walk(const V *v, int PM, int p, int h, V H, V &rho, bool &err) {
     V lim = H + base;
     V F1 = v[o.F1];
     if (F1 > lim) {
-        /* stops inside the first (partial) job: first x in [h, p-1] with
-         * P1[x+1] > lim, where P1[x+1] = P[x+1] for x < p-1 */
+        /* stops inside the first (partial) job: the last x in [h, p-1] with
+         * P[x] <= lim (P is non-decreasing; P[h] = base <= lim) */
         int x = h;
-        for (int y = h + 1; y < p; y++) x += (P[y] <= lim) ? 1 : 0;
+        for (int st = half; st > 0; st >>= 1) {
+            int y = x + st;
+            if (y <= p - 1 && P[y] <= lim) x = y;
+        }
         V tail = lim - P[x];
         V ex = e[x];
         if (ex > tail) {
@@ -378,33 +429,35 @@ RT_HD V walk(const V *v, int PM, int p, int h, V H, V &rho, bool &err) {
     }
     V w = EP[p] - EP[h];
     V H2 = lim - F1; /* H minus the first job's span */
+    int x = 0;
+    V Hs;
     if (v[o.WN] != 0) {
         /* negative wrap: the walk raises iff it reaches index 2p-1 */
         if (P[p - 1] <= H2) {
             err = true;
             return 0;
         }
-        int x = 0;
-        for (int y = 1; y < p - 1; y++) x += (P[y] <= H2) ? 1 : 0;
-        V tail = H2 - P[x];
-        if (e[x] > tail) {
-            rho = e[x] - tail;
-            return w + EP[x] + tail;
+        for (int st = half; st > 0; st >>= 1) {
+            int y = x + st;
+            if (y <= p - 2 && P[y] <= H2) x = y;
         }
-        return w + EP[x] + e[x];
+        Hs = H2;
+    } else {
+        V C = P[p];
+        if (C <= 0) {
+            /* all-zero period: the reference loops forever */
+            err = true;
+            return 0;
+        }
+        V k = Num<V>::floordiv(H2, C);
+        Hs = H2 - k * C;
+        w += k * EP[p];
+        for (int st = half; st > 0; st >>= 1) {
+            int y = x + st;
+            if (y <= p - 1 && P[y] <= Hs) x = y;
+        }
     }
-    V C = P[p];
-    if (C <= 0) {
-        /* all-zero period: the reference loops forever */
-        err = true;
-        return 0;
-    }
-    V k = Num<V>::floordiv(H2, C);
-    V H3 = H2 - k * C;
-    w += k * EP[p];
-    int x = 0;
-    for (int y = 1; y < p; y++) x += (P[y] <= H3) ? 1 : 0;
-    V tail = H3 - P[x];
+    V tail = Hs - P[x];
     if (e[x] > tail) {
         rho = e[x] - tail;
         return w + EP[x] + tail;
@@ -414,34 +467,41 @@ RT_HD V walk(const V *v, int PM, int p, int h, V H, V &rho, bool &err) {
 
 /* Sum over hp(k) of max over start segments of W (analysis.py:131
  * _max_workload summed as in mem_response / cpu_response). */
+#ifdef RT_COUNTERS
+extern long long g_cnt_interf[2], g_cnt_lfp[2], g_cnt_eval, g_cnt_views, g_cnt_rounds;
+#define RT_COUNT(x) (x)++
+#else
+#define RT_COUNT(x)
+#endif
+
 template <class V, class TM>
-RT_HD V interference(const TM &tm, SetCtx<V> &c, int k, int kind, V H, V &rho, bool &err) {
+RT_NI V interference(const TM &tm, SetCtx<V> &c, int k, int kind, V H, V &rho, bool &err) {
+    RT_COUNT(g_cnt_interf[kind]);
     rho = 0;
     err = false;
     if (H <= 0 || k == 0) return 0;
-    const int G = kind == K_CPU ? c.GC : c.GM;
-    const int tpr = 32 / G;
+    const int lg = kind == K_CPU ? c.lgC : c.lgM; /* lanes per task = 2^lg */
     const int PM = kind == K_CPU ? c.MC : c.MP;
+    const int half = kind == K_CPU ? c.halfC : c.halfM;
     const int stride = kind == K_CPU ? c.L.SC : c.L.SM;
     const V *views = kind == K_CPU ? c.vc : c.vm;
     const i64 prio_k = c.tr[k].prio;
-    V total = 0;
-    for (int i0 = 0; i0 < k; i0 += tpr) {
-        V ws, rm;
-        bool e;
-        tm.group_reduce(G, [&](int slot, V &w, V &r, bool &es) {
-            int i = i0 + slot / G, h = slot % G;
+    typename TM::template Acc<V> acc;
+    tm.acc_init(acc);
+    for (int i0 = 0; i0 < k; i0 += (32 >> lg)) {
+        RT_COUNT(g_cnt_rounds);
+        tm.group_max_round(lg, [&](int slot, V &w, V &r, bool &es) {
+            int i = i0 + (slot >> lg), h = slot & ((1 << lg) - 1);
             if (i < k) {
                 const TaskRec &ti = c.tr[i];
                 int p = kind == K_CPU ? ti.m : ti.p;
                 if (h < p && ti.prio < prio_k)
-                    w = walk(views + (size_t)i * stride, PM, p, h, H, r, es);
+                    w = walk(views + (size_t)i * stride, PM, half, p, h, H, r, es);
             }
-        }, ws, rm, e);
-        total += ws;
-        if (rm > rho) rho = rm;
-        if (e) err = true;
+        }, acc);
     }
+    V total;
+    tm.acc_finish(lg, acc, total, rho, err);
     return total;
 }
 
@@ -449,7 +509,8 @@ RT_HD V interference(const TM &tm, SetCtx<V> &c, int k, int kind, V H, V &rho, b
  * <= lfp).  Returns -1 for the reference's None (suspension.py:123: iterate
  * beyond the bound, or an InfeasibleGapError inside the interference). */
 template <class V, class TM>
-RT_HD V lfp(const TM &tm, SetCtx<V> &c, int k, int kind, V base, V start, V bound) {
+RT_NI V lfp(const TM &tm, SetCtx<V> &c, int k, int kind, V base, V start, V bound) {
+    RT_COUNT(g_cnt_lfp[kind]);
     if (base > bound) return (V)-1;
     V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
@@ -472,7 +533,7 @@ RT_HD V lfp(const TM &tm, SetCtx<V> &c, int k, int kind, V base, V start, V boun
  * warm starts: lfp(b') >= lfp(b) + (b' - b) for b' >= b, and None(b) implies
  * None(b') (both monotone).  Results in out[] (-1 = None). */
 template <class V, class TM>
-RT_HD void lfp_many(const TM &tm, SetCtx<V> &c, int k, int kind, const V *bases, V *out, int cnt,
+RT_NI void lfp_many(const TM &tm, SetCtx<V> &c, int k, int kind, const V *bases, V *out, int cnt,
                     V bound, bool stop_on_none, bool &any_none) {
     any_none = false;
     for (int j = 0; j < cnt; j++) {
@@ -538,7 +599,7 @@ RT_HD V sum_grup(const SetCtx<V> &c, int k, int g, typename Num<V>::Qt q) {
  * be null) receive per-segment numerators at scale q.
  */
 template <class V, class TM>
-RT_HD void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::Qt lcm_pre,
+RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::Qt lcm_pre,
                      bool want_all, TaskEval<V> &res, V *mr_out, V *cr_out) {
     typedef Num<V> N;
     const TaskRec &t = c.tr[k];
@@ -548,6 +609,7 @@ RT_HD void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
     res.e2e = res.r1 = res.r2 = (V)-1;
     if (c.esc) return;
     c.evals++;
+    RT_COUNT(g_cnt_eval);
     ensure_views(tm, c, k, q);
     const V D = N::sc(t.D, q);
     V *bases = c.scr;
@@ -605,7 +667,7 @@ RT_HD void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
  * minimum count of analysis.py:239 _min_feasible_gn in closed form:
  * sum_j[(gw_hi*a - gl*A)/(2*A*gn) + gl] + sum ml_hi + sum cl_hi <= D. */
 template <class V>
-RT_HD void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
+RT_NI void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
     const i64 *r = c.blob + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
     TaskRec &t = c.tr[i];
     t.m = (int)r[0];
@@ -704,7 +766,7 @@ template <class V> struct OutPtrs {
  * first failing task when stop_at_fail (the reference's per_task then holds
  * the tasks up to it).  Values are written as numerators over den[k]. */
 template <class V, class TM>
-RT_HD bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool stop_at_fail) {
+RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool stop_at_fail) {
     typedef typename Num<V>::Qt Qt;
     Qt lcm_pre = 1;
     V *mr = c.scr + 2 * (c.MP + c.MC + 2);
@@ -814,7 +876,7 @@ RT_HD void set_g(const TM &tm, SetCtx<V> &c, int k, int g) {
 
 /* smallest passing count in [lo, hi] for task k (own-count monotone), or 0 */
 template <class V, class TM>
-RT_HD int find_g(const TM &tm, SetCtx<V> &c, int k, int lo, int hi, typename Num<V>::Qt lcm_pre) {
+RT_NI int find_g(const TM &tm, SetCtx<V> &c, int k, int lo, int hi, typename Num<V>::Qt lcm_pre) {
     TaskEval<V> r;
     eval_task(tm, c, k, lo, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
     if (c.esc) return 0;
@@ -835,7 +897,7 @@ RT_HD int find_g(const TM &tm, SetCtx<V> &c, int k, int lo, int hi, typename Num
 /* Greedy descent (regular sets): equals the lexicographically first
  * schedulable allocation of the reference grid search. */
 template <class V, class TM>
-RT_HD int search_greedy(const TM &tm, SetCtx<V> &c) {
+RT_NI int search_greedy(const TM &tm, SetCtx<V> &c) {
     typedef typename Num<V>::Qt Qt;
     Qt lcm_pre = 1;
     i64 used = 0, rest_min = 0;
@@ -868,7 +930,7 @@ RT_HD int search_greedy(const TM &tm, SetCtx<V> &c) {
 
 /* Exact depth-first search with prefix pruning (irregular sets). */
 template <class V, class TM>
-RT_HD int search_dfs(const TM &tm, SetCtx<V> &c) {
+RT_NI int search_dfs(const TM &tm, SetCtx<V> &c) {
     typedef typename Num<V>::Qt Qt;
     int d = 0;
     for (;;) {

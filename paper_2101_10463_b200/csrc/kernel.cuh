@@ -26,8 +26,15 @@ struct KParams {
     i64 *esc0, *esc1;        /* escalation lists (stage 0 -> 1, 1 -> 2) */
 };
 
+/* minimum resident CTAs per SM the register allocation must allow */
+#ifndef RTGPU_MINB
+#define RTGPU_MINB 4
+#endif
+template <class V> struct MinBlocks { static constexpr int value = RTGPU_MINB; };
+template <> struct MinBlocks<i128> { static constexpr int value = 2; };
+
 template <class V>
-__global__ void __launch_bounds__(256) analyze_kernel(KParams p, int stage) {
+__global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KParams p, int stage) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -43,8 +50,7 @@ __global__ void __launch_bounds__(256) analyze_kernel(KParams p, int stage) {
     c.maxn = p.dims.maxn;
     c.MC = p.dims.MC;
     c.MP = p.dims.MP;
-    c.GC = p.GC;
-    c.GM = p.GM;
+    set_groups(c);
     c.budget = p.budget;
     WarpTeam tm{lane};
     const i64 count = stage == 0 ? p.n_sets : (i64)(stage == 1 ? p.ctr[3] : p.ctr[4]);

@@ -35,12 +35,7 @@ int run_one(const Dims &d, const i64 *blob, unsigned flags, i64 budget, OutPtrs<
     c.maxn = d.maxn;
     c.MC = d.MC;
     c.MP = d.MP;
-    int g = 1;
-    while (g < d.MC) g <<= 1;
-    c.GC = g;
-    g = 1;
-    while (g < (d.MP > 0 ? d.MP : 1)) g <<= 1;
-    c.GM = g;
+    set_groups(c);
     c.budget = budget > 0 ? budget : (i64)1 << 22;
     SeqTeam tm;
     int st = analyze_set(tm, c, flags, o);
