@@ -177,6 +177,8 @@ template <class V> struct SetCtx {
     i64 A;
     int maxn, MC, MP, GC, GM; /* batch maxima, lane group sizes */
     int lgC, lgM, halfC, halfM; /* log2 group sizes; binary-search first steps */
+    int single_seg;     /* busy-waiting baseline: one CPU segment per task */
+    int method;         /* RTGPU_METHOD_* */
     i64 Vb;             /* range bound in input ticks */
     Qt qlim;            /* largest admissible scale: limit / Vb */
     /* current views: tasks [0, vn) at scale vq */
@@ -327,6 +329,27 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
     const i64 *gw_lo = ml_hi + p;
     typename Num<V>::Qt perlo = t.isgpu ? q / (2 * (typename Num<V>::Qt)t.g) : q;
+    if (c.single_seg) {
+        /* busy-waiting baseline (analysis.py:360): one execution segment of
+         * length sum(CL up) + sum(ML up) + sum(GR up), no suspension */
+        VOff o(c.MC);
+        V *v = c.vc + (size_t)i * c.L.SC;
+        V gru = 0;
+        if (t.isgpu) {
+            typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * t.g);
+            gru = (V)t.sInfl * (V)per + Num<V>::sc(t.sGL, q);
+        }
+        V e = N::sc(t.sClu + t.sMlu, q) + gru;
+        v[o.e] = e;
+        v[o.P] = 0;
+        v[o.EP] = 0;
+        v[o.EP + 1] = e;
+        v[o.F1] = e + N::sc(t.T - t.D, q);
+        V wrap = N::sc(t.T, q) - e;
+        v[o.WN] = wrap < 0 ? (V)1 : (V)0;
+        v[o.P + 1] = e + (wrap < 0 ? (V)0 : wrap);
+        return;
+    }
     /* CPU chain */
     {
         VOff o(c.MC);
@@ -474,29 +497,49 @@ extern long long g_cnt_interf[2], g_cnt_lfp[2], g_cnt_eval, g_cnt_views, g_cnt_r
 #define RT_COUNT(x)
 #endif
 
+/* What the interference loop reads, copied out of the set context so the
+ * hot loop keeps it in registers (no aliasing with shared-memory writes). */
+template <class V> struct IView {
+    const TaskRec *tr;
+    const V *views;
+    int k, kind, lg, PM, half, stride, p1;
+    i64 prio_k;
+};
+
+template <class V>
+RT_HD IView<V> make_iview(const SetCtx<V> &c, int k, int kind) {
+    IView<V> v;
+    v.tr = c.tr;
+    v.k = k;
+    v.kind = kind;
+    v.lg = kind == K_CPU ? c.lgC : c.lgM;
+    v.PM = kind == K_CPU ? c.MC : c.MP;
+    v.half = kind == K_CPU ? c.halfC : c.halfM;
+    v.stride = kind == K_CPU ? c.L.SC : c.L.SM;
+    v.views = kind == K_CPU ? c.vc : c.vm;
+    v.p1 = c.single_seg;
+    v.prio_k = c.tr[k].prio;
+    return v;
+}
+
 template <class V, class TM>
-RT_NI V interference(const TM &tm, SetCtx<V> &c, int k, int kind, V H, V &rho, bool &err) {
-    RT_COUNT(g_cnt_interf[kind]);
+RT_HD V interference(const TM &tm, const IView<V> &iv, V H, V &rho, bool &err) {
+    RT_COUNT(g_cnt_interf[iv.kind]);
     rho = 0;
     err = false;
-    if (H <= 0 || k == 0) return 0;
-    const int lg = kind == K_CPU ? c.lgC : c.lgM; /* lanes per task = 2^lg */
-    const int PM = kind == K_CPU ? c.MC : c.MP;
-    const int half = kind == K_CPU ? c.halfC : c.halfM;
-    const int stride = kind == K_CPU ? c.L.SC : c.L.SM;
-    const V *views = kind == K_CPU ? c.vc : c.vm;
-    const i64 prio_k = c.tr[k].prio;
+    if (H <= 0 || iv.k == 0) return 0;
     typename TM::template Acc<V> acc;
     tm.acc_init(acc);
-    for (int i0 = 0; i0 < k; i0 += (32 >> lg)) {
+    const int lg = iv.lg;
+    for (int i0 = 0; i0 < iv.k; i0 += (32 >> lg)) {
         RT_COUNT(g_cnt_rounds);
         tm.group_max_round(lg, [&](int slot, V &w, V &r, bool &es) {
             int i = i0 + (slot >> lg), h = slot & ((1 << lg) - 1);
-            if (i < k) {
-                const TaskRec &ti = c.tr[i];
-                int p = kind == K_CPU ? ti.m : ti.p;
-                if (h < p && ti.prio < prio_k)
-                    w = walk(views + (size_t)i * stride, PM, half, p, h, H, r, es);
+            if (i < iv.k) {
+                const TaskRec &ti = iv.tr[i];
+                int p = iv.kind == K_CPU ? (iv.p1 ? 1 : ti.m) : ti.p;
+                if (h < p && ti.prio < iv.prio_k)
+                    w = walk(iv.views + (size_t)i * iv.stride, iv.PM, iv.half, p, h, H, r, es);
             }
         }, acc);
     }
@@ -512,11 +555,12 @@ template <class V, class TM>
 RT_NI V lfp(const TM &tm, SetCtx<V> &c, int k, int kind, V base, V start, V bound) {
     RT_COUNT(g_cnt_lfp[kind]);
     if (base > bound) return (V)-1;
+    const IView<V> iv = make_iview(c, k, kind);
     V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
         V rho;
         bool err;
-        V I = interference(tm, c, k, kind, r, rho, err);
+        V I = interference(tm, iv, r, rho, err);
         if (err) return (V)-1;
         V nxt = base + I;
         if (nxt <= r) return r; /* nxt == r in exact arithmetic */
@@ -985,6 +1029,282 @@ RT_NI int search_dfs(const TM &tm, SetCtx<V> &c) {
     }
 }
 
+/* ------------------------------------------------------------ baselines */
+
+template <class V> RT_HD i64 out_num(V v) { return v < 0 ? (i64)RTGPU_NONE : (i64)Num<V>::wide(v); }
+
+/* Baselines of analysis.py:319 (self-suspension) and :355 (busy-waiting),
+ * evaluated on a full allocation tr[].g at one scale q = 2*A*lcm(g).
+ * Each task becomes a SuspTask (suspension.py:23); task_response
+ * (suspension.py:155) uses the CPU chain views: self-suspension gaps are the
+ * memory+kernel spans' lower bounds -- the same gaps as the RTGPU CPU chain
+ * -- and busy-waiting collapses a task to one segment. */
+
+/* sum over kernels of GR up at scale q (0 for pure-CPU tasks) */
+template <class V> RT_HD V grup_at(const SetCtx<V> &c, const TaskRec &t, int gcount, typename Num<V>::Qt q) {
+    if (!t.isgpu) return 0;
+    typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * gcount);
+    return (V)t.sInfl * (V)per + Num<V>::sc(t.sGL, q);
+}
+
+/* Largest suspension-interval upper bound of task t at scale q (the
+ * self-suspension blocking a higher-priority task can suffer from it). */
+template <class V> RT_HD V max_susp_hi(const SetCtx<V> &c, const TaskRec &t, int gcount, typename Num<V>::Qt q) {
+    if (!t.isgpu) return 0;
+    const i64 *sg = c.blob + t.seg;
+    const int m = t.m, p = t.p, g = m - 1;
+    const i64 *ml_hi = sg + 2 * m + p, *gw_hi = sg + 2 * m + 2 * p + g, *gl = gw_hi + g, *an = gl + g;
+    typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * gcount);
+    V best = 0;
+    for (int j = 0; j < g; j++) {
+        V gr = (V)((i128)gw_hi[j] * an[j] - (i128)gl[j] * c.A) * (V)per + Num<V>::sc(gl[j], q);
+        V m1 = c.mm == RTGPU_TWO_COPY ? Num<V>::sc(ml_hi[2 * j] + ml_hi[2 * j + 1], q)
+                                      : Num<V>::sc(ml_hi[j], q);
+        best = tmax(best, m1 + gr);
+    }
+    return best;
+}
+
+/* SuspTask validity (suspension.py:35) of task t under its count, exact:
+ * every lo <= hi, and sum(exec hi) + sum(susp lo) <= T. */
+template <class V> RT_HD bool susp_valid(const SetCtx<V> &c, const TaskRec &t, int gcount, typename Num<V>::Qt q) {
+    const i64 *sg = c.blob + t.seg;
+    const int m = t.m, p = t.p, g = m - 1;
+    const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
+    const i64 *gw_lo = ml_hi + p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+    typename Num<V>::Qt perlo = t.isgpu ? q / (2 * (typename Num<V>::Qt)gcount) : q;
+    typename Num<V>::Qt perhi =
+        t.isgpu ? q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * gcount) : q;
+    auto grl = [&](int j) { return (V)gw_lo[j] * (V)perlo; };
+    auto gru = [&](int j) {
+        return (V)((i128)gw_hi[j] * an[j] - (i128)gl[j] * c.A) * (V)perhi + Num<V>::sc(gl[j], q);
+    };
+    if (c.method == RTGPU_METHOD_BUSYWAIT) {
+        V lo = Num<V>::sc(t.sCll + t.sMll, q), hi = Num<V>::sc(t.sClu + t.sMlu, q);
+        for (int j = 0; j < g; j++) {
+            lo += grl(j);
+            hi += gru(j);
+        }
+        return lo <= hi && hi <= Num<V>::sc(t.T, q);
+    }
+    for (int j = 0; j < m; j++)
+        if (cl_lo[j] > cl_hi[j]) return false;
+    V sl_sum = 0;
+    for (int j = 0; j < g; j++) {
+        V lo, hi;
+        if (c.mm == RTGPU_TWO_COPY) {
+            lo = Num<V>::sc(ml_lo[2 * j] + ml_lo[2 * j + 1], q) + grl(j);
+            hi = Num<V>::sc(ml_hi[2 * j] + ml_hi[2 * j + 1], q) + gru(j);
+        } else {
+            lo = Num<V>::sc(ml_lo[j], q) + grl(j);
+            hi = Num<V>::sc(ml_hi[j], q) + gru(j);
+        }
+        if (lo > hi) return false;
+        sl_sum += lo;
+    }
+    return Num<V>::sc(t.sClu, q) + sl_sum <= Num<V>::sc(t.T, q);
+}
+
+/* task_response (suspension.py:155) of task k with blocking B at scale q;
+ * verdict mode computes R2 first and R1 only if needed.  Returns -1 = None. */
+template <class V, class TM>
+RT_NI V baseline_response(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt q, V B,
+                          bool want_all) {
+    const TaskRec &t = c.tr[k];
+    const V D = Num<V>::sc(t.D, q);
+    V sum_sh = 0, sum_eh;
+    if (c.single_seg) {
+        sum_eh = Num<V>::sc(t.sClu + t.sMlu, q) + grup_at(c, t, t.g, q);
+    } else {
+        sum_eh = Num<V>::sc(t.sClu, q);
+        if (t.isgpu) sum_sh = Num<V>::sc(t.sMlu, q) + grup_at(c, t, t.g, q);
+    }
+    V r2 = lfp(tm, c, k, K_CPU, sum_sh + sum_eh + B, sum_sh + sum_eh + B, D);
+    if (c.single_seg) return r2; /* one segment, no suspension: R1 == R2 */
+    if (r2 >= 0 && !want_all) return r2;
+    V *bases = c.scr;
+    V *outs = c.scr + (c.MP + c.MC + 2);
+    const i64 *cl_hi = c.blob + t.seg + t.m;
+    tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q) + B; });
+    bool none;
+    lfp_many(tm, c, k, K_CPU, bases, outs, t.m, D, true, none);
+    V r1 = (V)-1;
+    if (!none) {
+        V acc = sum_sh;
+        for (int j = 0; j < t.m; j++) acc += outs[j];
+        if (acc <= D) r1 = acc;
+    }
+    tm.sync();
+    if (r1 < 0) return r2;
+    if (r2 < 0) return r1;
+    return tmin(r1, r2);
+}
+
+/* scale of a full allocation: 2*A*lcm(all GPU counts) (1 without GPU tasks) */
+template <class V> RT_HD typename Num<V>::Qt alloc_scale(SetCtx<V> &c) {
+    typedef typename Num<V>::Qt Qt;
+    Qt L = 1;
+    bool any = false;
+    for (int i = 0; i < c.n; i++)
+        if (c.tr[i].isgpu) {
+            any = true;
+            L = lcm_lim<Qt>(L, (Qt)c.tr[i].g, c.qlim);
+            if (L == 0) break;
+        }
+    if (!any) return 1;
+    if (L == 0 || L > c.qlim / (2 * (Qt)c.A)) {
+        c.esc = 1;
+        return 0;
+    }
+    return L * 2 * (Qt)c.A;
+}
+
+/* Evaluate the current full allocation (analysis.py:323-350 / 360-390).
+ * Returns n if every task passes, else the index of the first failing task,
+ * or -1 if some task is not a valid SuspTask (evaluate returns (False, {})).
+ * With out != null (report), writes e2e / den / GR detail per task. */
+template <class V, class TM>
+RT_NI int eval_alloc_baseline(const TM &tm, SetCtx<V> &c, bool want_all, const OutPtrs<V> *out) {
+    typedef typename Num<V>::Qt Qt;
+    Qt q = alloc_scale(c);
+    if (c.esc) return -2;
+    c.vn = 0;
+    ensure_views(tm, c, c.n, q);
+    for (int i = 0; i < c.n; i++)
+        if (!susp_valid(c, c.tr[i], c.tr[i].g, q)) return -1;
+    for (int k = 0; k < c.n; k++) {
+        c.evals++;
+        V B = 0;
+        if (c.method == RTGPU_METHOD_SELFSUSP)
+            for (int i = 0; i < c.n; i++)
+                if (c.tr[i].prio > c.tr[k].prio) B = tmax(B, max_susp_hi(c, c.tr[i], c.tr[i].g, q));
+        V r = baseline_response(tm, c, k, q, B, want_all);
+        if (c.esc || c.stuck) return -2;
+        if (out) {
+            const TaskRec &t = c.tr[k];
+            tm.sync();
+            if (sizeof(V) > 8 && ((i128)q > (i128)INT64_MAX || Num<V>::wide(r) > (i128)INT64_MAX)) {
+                c.esc = 1;
+                return -2;
+            }
+            if (tm.leader()) {
+                out->e2e[k] = out_num(r);
+                out->den[k] = (i64)q;
+            }
+            if (out->detail && t.isgpu) {
+                const i64 *sg = c.blob + t.seg;
+                const int m = t.m, p = t.p, g = m - 1;
+                const i64 *gw_lo = sg + 2 * m + 2 * p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+                i64 *d = out->detail + t.seg;
+                const Qt perlo = q / (2 * (Qt)t.g), perhi = q / (2 * (Qt)c.A * (Qt)t.g);
+                tm.pfor(g, [&](int j) {
+                    d[2 * m + 2 * p + j] = out_num((V)gw_lo[j] * (V)perlo);
+                    V infl = (V)((i128)gw_hi[j] * an[j] - (i128)gl[j] * c.A);
+                    d[2 * m + 2 * p + g + j] = out_num(infl * (V)perhi + Num<V>::sc(gl[j], q));
+                });
+            }
+        }
+        if (r < 0) return k;
+    }
+    return c.n;
+}
+
+/* smallest count >= lo at which task t is a valid SuspTask (monotone), 0 if none */
+template <class V> RT_HD int min_valid_g(SetCtx<V> &c, int k, int lo) {
+    typedef typename Num<V>::Qt Qt;
+    const TaskRec &t = c.tr[k];
+    for (int g = lo; g <= c.GN; g++) {
+        Qt q = (Qt)2 * (Qt)c.A * (Qt)g;
+        if (q > c.qlim) {
+            c.esc = 1;
+            return 0;
+        }
+        if (susp_valid(c, t, g, q)) return g;
+    }
+    return 0;
+}
+
+/* Lexicographic enumeration of analysis.py:250 _grid_search for the
+ * baselines with sound pruning: allocations below a task's validity minimum
+ * are skipped (they fail in evaluate), and when task f fails, every
+ * allocation sharing the counts of GPU tasks up to f is skipped if f fails
+ * regardless of the rest -- always for busy-waiting (no blocking term), and
+ * for self-suspension when f also fails under the smallest blocking any
+ * completion can give (each lp kernel span is at least its copies + GL). */
+template <class V, class TM>
+RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
+    int ids[RTGPU_MAX_TASKS], lower[RTGPU_MAX_TASKS], nid = 0;
+    for (int k = 0; k < c.n; k++)
+        if (c.tr[k].isgpu) {
+            int g = min_valid_g(c, k, c.tr[k].gmin);
+            if (c.esc) return ST_ESCALATE;
+            if (g == 0) return RTGPU_UNSCHEDULABLE;
+            ids[nid] = k;
+            lower[nid++] = g;
+        }
+    i64 need = 0;
+    for (int q = 0; q < nid; q++) need += lower[q];
+    if (need > c.GN) return RTGPU_UNSCHEDULABLE;
+    tm.sync();
+    if (tm.leader())
+        for (int q = 0; q < nid; q++) c.tr[ids[q]].g = lower[q];
+    tm.sync();
+    for (;;) {
+        if (c.budget > 0 && c.evals >= c.budget) return RTGPU_UNDECIDED;
+        int f = eval_alloc_baseline(tm, c, false, (const OutPtrs<V> *)nullptr);
+        if (c.esc) return ST_ESCALATE;
+        if (c.stuck) return RTGPU_UNDECIDED;
+        if (f == c.n) return RTGPU_SCHEDULABLE;
+        int pos = nid - 1; /* odometer position to advance */
+        if (f >= 0) {
+            bool prefix_dead = c.method == RTGPU_METHOD_BUSYWAIT;
+            if (!prefix_dead) {
+                /* self-suspension: retry f with the smallest possible blocking */
+                typedef typename Num<V>::Qt Qt;
+                Qt q = alloc_scale(c);
+                if (c.esc) return ST_ESCALATE;
+                V Bmin = 0;
+                for (int i = 0; i < c.n; i++) {
+                    const TaskRec &t = c.tr[i];
+                    if (t.prio <= c.tr[f].prio || !t.isgpu) continue;
+                    const i64 *sg = c.blob + t.seg;
+                    const int m = t.m, p = t.p, g = m - 1;
+                    const i64 *ml_hi = sg + 2 * m + p, *gl = sg + 2 * m + 2 * p + 2 * g;
+                    for (int j = 0; j < g; j++) {
+                        i64 x = c.mm == RTGPU_TWO_COPY ? ml_hi[2 * j] + ml_hi[2 * j + 1] : ml_hi[j];
+                        Bmin = tmax(Bmin, Num<V>::sc(x + gl[j], q));
+                    }
+                }
+                V r = baseline_response(tm, c, f, q, Bmin, false);
+                if (c.esc) return ST_ESCALATE;
+                prefix_dead = r < 0;
+            }
+            if (prefix_dead) {
+                pos = -1;
+                for (int q = 0; q < nid; q++)
+                    if (ids[q] <= f) pos = q;
+                if (pos < 0) return RTGPU_UNSCHEDULABLE; /* fails before any choice */
+            }
+        }
+        /* advance the odometer at pos (gpu.py:43 order) */
+        int q = pos;
+        for (; q >= 0; q--) {
+            i64 used = 0, after = 0;
+            for (int a = 0; a < q; a++) used += c.tr[ids[a]].g;
+            for (int a = q + 1; a < nid; a++) after += lower[a];
+            if (c.tr[ids[q]].g + 1 <= c.GN - used - after) break;
+        }
+        if (q < 0) return RTGPU_UNSCHEDULABLE;
+        tm.sync();
+        if (tm.leader()) {
+            c.tr[ids[q]].g += 1;
+            for (int a = q + 1; a < nid; a++) c.tr[ids[a]].g = lower[a];
+        }
+        tm.sync();
+        c.vn = 0;
+    }
+}
+
 /* Whole pipeline for one set; returns the status (or ST_ESCALATE). */
 template <class V, class TM>
 RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<V> &o) {
@@ -1000,6 +1320,7 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
     c.stuck = 0;
     c.evals = 0;
     c.budget_hit = 0;
+    c.single_seg = c.method == RTGPU_METHOD_BUSYWAIT;
     tm.pfor(c.n, [&](int i) {
         o.vsm[i] = 0;
         o.e2e[i] = RTGPU_ABSENT;
@@ -1045,7 +1366,8 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
             if (c.tr[i].prio > c.tr[k].prio) b = tmax(b, c.tr[i].maxMlu);
         c.tr[k].B = b;
     });
-    int st = irregular ? search_dfs(tm, c) : search_greedy(tm, c);
+    const bool rtg = c.method == RTGPU_METHOD_RTGPU;
+    int st = !rtg ? search_baseline(tm, c) : irregular ? search_dfs(tm, c) : search_greedy(tm, c);
     if (st == ST_ESCALATE) return st;
     if (st == RTGPU_SCHEDULABLE) {
         tm.pfor(c.n, [&](int i) { o.vsm[i] = c.tr[i].isgpu ? 2 * c.tr[i].g : 0; });
@@ -1070,7 +1392,18 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
             c.vn = 0;
         }
         c.stuck = 0;
-        report_pass(tm, c, o, st == RTGPU_UNSCHEDULABLE);
+        if (rtg) {
+            report_pass(tm, c, o, st == RTGPU_UNSCHEDULABLE);
+        } else {
+            int f = eval_alloc_baseline(tm, c, true, &o);
+            if (f >= 0) /* tasks after the first failing one are not in per_task */
+                for (int k = f + 1; k < c.n; k++)
+                    if (tm.leader()) {
+                        o.e2e[k] = RTGPU_ABSENT;
+                        o.den[k] = 1;
+                    }
+            tm.sync();
+        }
         if (c.esc) return ST_ESCALATE;
         if (c.stuck) return RTGPU_UNDECIDED;
     }

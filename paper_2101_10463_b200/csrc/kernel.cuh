@@ -17,6 +17,7 @@ struct KParams {
     Dims dims;
     int GC, GM;
     unsigned flags;
+    int method;
     i64 budget;
     int32_t *status;
     i64 *evals;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
     c.MP = p.dims.MP;
     set_groups(c);
     c.budget = p.budget;
+    c.method = p.method;
     WarpTeam tm{lane};
     const i64 count = stage == 0 ? p.n_sets : (i64)(stage == 1 ? p.ctr[3] : p.ctr[4]);
     const i64 *list = stage == 0 ? nullptr : (stage == 1 ? p.esc0 : p.esc1);

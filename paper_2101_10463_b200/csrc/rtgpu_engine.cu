@@ -84,8 +84,8 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
                const Dims &dims, int method, unsigned flags, i64 budget, int32_t *d_status,
                i64 *d_evals, int32_t *d_vsm, i64 *d_e2e, i64 *d_den, i64 *d_detail,
                cudaStream_t st) {
-    if (method != RTGPU_METHOD_RTGPU) {
-        snprintf(g_err, sizeof g_err, "method %d not implemented by the engine", method);
+    if (method < RTGPU_METHOD_RTGPU || method > RTGPU_METHOD_BUSYWAIT) {
+        snprintf(g_err, sizeof g_err, "unknown analysis method %d", method);
         return -2;
     }
     g_launches = 0;
@@ -104,6 +104,7 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     p.GC = pow2_group(dims.MC);
     p.GM = pow2_group(dims.MP > 0 ? dims.MP : 1);
     p.flags = flags;
+    p.method = method;
     p.budget = budget > 0 ? budget : (i64)1 << 22;
     p.status = d_status;
     p.evals = d_evals;

@@ -1,5 +1,5 @@
 # A/B of library variants: default build vs variants/*.so, bench only (+ one ncu of default)
-for v in default variants/lib_minb3.so variants/lib_minb2.so; do
+for v in default variants/lib_minb3.so; do
   if [ "$v" = default ]; then unset RTGPU_LIB; else export RTGPU_LIB=$PWD/$v; fi
   echo "== $v"
   timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d['value']), 'sets/s', 'k0_ms', round(d['roofline']['kernel_ms'],2), d['clocks'])"

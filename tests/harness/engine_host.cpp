@@ -20,7 +20,7 @@ using namespace rtgpu;
 namespace {
 
 template <class V>
-int run_one(const Dims &d, const i64 *blob, unsigned flags, i64 budget, OutPtrs<V> o, i64 *evals) {
+int run_one(const Dims &d, const i64 *blob, int method, unsigned flags, i64 budget, OutPtrs<V> o, i64 *evals) {
     Layout<V> L;
     L.init(d);
     std::vector<unsigned char> slab((size_t)L.bytes + 64);
@@ -37,6 +37,7 @@ int run_one(const Dims &d, const i64 *blob, unsigned flags, i64 budget, OutPtrs<
     c.MP = d.MP;
     set_groups(c);
     c.budget = budget > 0 ? budget : (i64)1 << 22;
+    c.method = method;
     SeqTeam tm;
     int st = analyze_set(tm, c, flags, o);
     *evals = c.evals;
@@ -46,7 +47,7 @@ int run_one(const Dims &d, const i64 *blob, unsigned flags, i64 budget, OutPtrs<
 }  // namespace
 
 extern "C" int host_analyze_batch(const int64_t *blobs, const int64_t *set_off,
-                                  const int64_t *task_base, int64_t n_sets, unsigned flags,
+                                  const int64_t *task_base, int64_t n_sets, int method, unsigned flags,
                                   int64_t budget, int first_stage, int32_t *status,
                                   int64_t *evals, int32_t *vsm, int64_t *e2e, int64_t *den,
                                   int64_t *detail, int32_t *stage_used) {
@@ -70,15 +71,15 @@ extern "C" int host_analyze_batch(const int64_t *blobs, const int64_t *set_off,
             if (stage == 0) {
                 OutPtrs<double> o{vsm + tb, (i64 *)e2e + tb, (i64 *)den + tb,
                                   detail ? (i64 *)detail + set_off[s] : nullptr};
-                st = run_one<double>(d, blob, flags, budget, o, &ev);
+                st = run_one<double>(d, blob, method, flags, budget, o, &ev);
             } else if (stage == 1) {
                 OutPtrs<i64> o{vsm + tb, (i64 *)e2e + tb, (i64 *)den + tb,
                                detail ? (i64 *)detail + set_off[s] : nullptr};
-                st = run_one<i64>(d, blob, flags, budget, o, &ev);
+                st = run_one<i64>(d, blob, method, flags, budget, o, &ev);
             } else {
                 OutPtrs<i128> o{vsm + tb, (i64 *)e2e + tb, (i64 *)den + tb,
                                 detail ? (i64 *)detail + set_off[s] : nullptr};
-                st = run_one<i128>(d, blob, flags, budget, o, &ev);
+                st = run_one<i128>(d, blob, method, flags, budget, o, &ev);
             }
             evals[s] = ev;
         }

@@ -30,7 +30,7 @@ def lib():
         _lib = ctypes.CDLL(LIB)
         p64 = ctypes.POINTER(ctypes.c_int64)
         p32 = ctypes.POINTER(ctypes.c_int32)
-        _lib.host_analyze_batch.argtypes = [p64, p64, p64, ctypes.c_int64, ctypes.c_uint,
+        _lib.host_analyze_batch.argtypes = [p64, p64, p64, ctypes.c_int64, ctypes.c_int, ctypes.c_uint,
                                             ctypes.c_int64, ctypes.c_int, p32, p64, p32, p64,
                                             p64, p64, p32]
     return _lib
@@ -40,7 +40,7 @@ def _p(a, t):
     return a.ctypes.data_as(ctypes.POINTER(t)) if a is not None else None
 
 
-def analyze_batch(blobs, set_off, task_base, flags=2, budget=0, first_stage=0, detail=True):
+def analyze_batch(blobs, set_off, task_base, flags=2, budget=0, first_stage=0, detail=True, method=0):
     S = len(set_off) - 1
     T = int(task_base[-1])
     out = dict(status=np.zeros(S, np.int32), evals=np.zeros(S, np.int64),
@@ -51,7 +51,7 @@ def analyze_batch(blobs, set_off, task_base, flags=2, budget=0, first_stage=0, d
     blobs = np.ascontiguousarray(blobs, np.int64)
     lib().host_analyze_batch(
         _p(blobs, ctypes.c_int64), _p(np.ascontiguousarray(set_off, np.int64), ctypes.c_int64),
-        _p(np.ascontiguousarray(task_base, np.int64), ctypes.c_int64), S, flags, budget,
+        _p(np.ascontiguousarray(task_base, np.int64), ctypes.c_int64), S, method, flags, budget,
         first_stage, _p(out["status"], ctypes.c_int32), _p(out["evals"], ctypes.c_int64),
         _p(out["vsm"], ctypes.c_int32), _p(out["e2e_num"], ctypes.c_int64),
         _p(out["den"], ctypes.c_int64), _p(out["detail"], ctypes.c_int64),

@@ -26,22 +26,27 @@ def golden():
     return cases, pack_tasksets([ts_from_exact(c["taskset"]) for c in cases])
 
 
+METHODS = [AnalysisMethod.RTGPU, AnalysisMethod.SELF_SUSPENSION, AnalysisMethod.BUSY_WAITING]
+
+
 @pytest.mark.parametrize("stage", [0, 1, 2])
-def test_engine_core_matches_reference_reports(golden, stage):
+@pytest.mark.parametrize("mi", [0, 1, 2])
+def test_engine_core_matches_reference_reports(golden, stage, mi):
     cases, batch = golden
+    method = METHODS[mi]
     out = harness.analyze_batch(batch.blobs, batch.set_off, batch.task_base, flags=2,
-                                first_stage=stage)
+                                first_stage=stage, method=mi)
     assert (out["stage"] == stage).all()
     res = RawResults(out["status"], out["evals"], out["vsm"], out["e2e_num"], out["den"],
                      out["detail"])
     bad = []
     for s, c in enumerate(cases):
-        want = c["rtgpu"]
+        want = c[method.value]
         if "raises" in want:
             if res.status[s] != INVALID:
                 bad.append(s)
             continue
-        if report_to_dict(unpack_report(batch, res, s, AnalysisMethod.RTGPU)) != want:
+        if report_to_dict(unpack_report(batch, res, s, method)) != want:
             bad.append(s)
     assert not bad, bad[:5]
 
@@ -57,12 +62,13 @@ def compare(o, h):
             assert Fraction(a, int(o["den"][i])) == Fraction(b, int(h["den"][i]))
 
 
+@pytest.mark.parametrize("mi", [0, 1, 2])
 @pytest.mark.parametrize("n,m,gn,u,mm", [(8, 5, 10, "2/5", 0), (5, 5, 10, "3/5", 1),
                                          (4, 3, 6, "1", 0), (6, 2, 12, "4/5", 1)])
-def test_engine_core_matches_oracle_generated(n, m, gn, u, mm):
+def test_engine_core_matches_oracle_generated(n, m, gn, u, mm, mi):
     gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), Fraction(u), mm,
                               gn, Fraction(12, 100), Fraction(1) if mm == 0 else Fraction(7, 10))
     b, so, tb = _native.generate(gp, list(range(120)))
-    o = oracle.analyze_batch(b, so, tb, flags=1, threads=8, detail=False)
-    h = harness.analyze_batch(b, so, tb, flags=1, detail=False)
+    o = oracle.analyze_batch(b, so, tb, method=mi, flags=1, threads=8, detail=False)
+    h = harness.analyze_batch(b, so, tb, method=mi, flags=1, detail=False)
     compare(o, h)

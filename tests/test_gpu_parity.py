@@ -27,24 +27,28 @@ def golden():
     return cases, pack_tasksets([ts_from_exact(c["taskset"]) for c in cases])
 
 
-def _check_golden(cases, batch, res):
+METHODS = [AnalysisMethod.RTGPU, AnalysisMethod.SELF_SUSPENSION, AnalysisMethod.BUSY_WAITING]
+
+
+def _check_golden(cases, batch, res, method=AnalysisMethod.RTGPU):
     bad = []
     for s, c in enumerate(cases):
-        want = c["rtgpu"]
+        want = c[method.value]
         if "raises" in want:
             if res.status[s] != INVALID:
                 bad.append(s)
             continue
-        if report_to_dict(unpack_report(batch, res, s, AnalysisMethod.RTGPU)) != want:
+        if report_to_dict(unpack_report(batch, res, s, method)) != want:
             bad.append(s)
     return bad
 
 
+@pytest.mark.parametrize("mi", [0, 1, 2])
 @pytest.mark.parametrize("first", [0, F_FIRST_I64, F_FIRST_I128])
-def test_gpu_matches_reference_reports(golden, first):
+def test_gpu_matches_reference_reports(golden, first, mi):
     cases, batch = golden
-    res = analyze_packed(batch.blobs, batch.set_off, batch.task_base, 0, F_DETAIL | first)
-    assert not _check_golden(cases, batch, res)
+    res = analyze_packed(batch.blobs, batch.set_off, batch.task_base, mi, F_DETAIL | first)
+    assert not _check_golden(cases, batch, res, METHODS[mi])
     assert _native.last_launch_count() == 3
 
 
@@ -67,6 +71,21 @@ def _cmp(o, g_status, g_vsm, g_e2e, g_den):
             assert a == b, i
         else:
             assert Fraction(a, int(o["den"][i])) == Fraction(b, int(g_den[i])), i
+
+
+@pytest.mark.parametrize("mi", [1, 2])
+@pytest.mark.parametrize("n,m,gn,u", [(8, 5, 10, "2/5"), (5, 3, 10, "1"), (6, 2, 12, "4/5")])
+def test_gpu_baselines_match_oracle(n, m, gn, u, mi):
+    gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), Fraction(u), 0,
+                              gn, Fraction(12, 100), Fraction(1))
+    b, so, tb = _native.generate(gp, [f"5:{u}:{i}" for i in range(300)])
+    o = oracle.analyze_batch(b, so, tb, method=mi, flags=1, threads=8, detail=False)
+    batch = DeviceBatch(b, so, tb)
+    out = batch.alloc_results()
+    batch.run(out, method=mi, flags=F_BOUNDS)
+    g = out.to_host()
+    _cmp({k: v for k, v in o.items() if k not in ("detail", "evals")},
+         g.status, g.vsm, g.e2e_num, g.den)
 
 
 @pytest.mark.parametrize("n,m,gn,u,mm,lo", [
