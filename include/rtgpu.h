@@ -133,6 +133,55 @@ int rtgpu_analyze_device(const int64_t *d_blobs, const int64_t *d_set_off,
                          int64_t *d_e2e_num, int64_t *d_den,
                          int64_t *d_detail, void *stream);
 
+/*
+ * Point queries: the analysis building blocks on packed sets, one query per
+ * warp.  The sets use the blob layout with explicit GPU response bounds:
+ * every kernel is packed with GW = [2*GR_lo, 2*GR_up], GL = 0, alpha = 1
+ * (alpha_den 1) and the engine gives it one physical SM, so Lemma 4 returns
+ * exactly [GR_lo, GR_up].  A SuspTask (suspension.py:23) is packed as a
+ * two-copy task whose copies carry its suspension bounds (even copies) and
+ * zero (odd copies), with zero-length kernels.  Results are numerators over
+ * den (a multiple of the input tick), RTGPU_NONE for None.
+ *
+ *   kind                      reference (file:line)            task / index / horizon / blocking
+ *   RTGPU_Q_WORKLOAD          suspension.workload:107          k / h / t / -
+ *   RTGPU_Q_MAX_WORKLOAD      suspension.max_workload:116      k / - / t / -
+ *   RTGPU_Q_SEGMENT_RESPONSE  suspension.segment_response:140  k / j / - / blocking (hp = prio < k)
+ *   RTGPU_Q_TASK_RESPONSE     suspension.task_response:155     k / - / - / blocking
+ *   RTGPU_Q_MEM_RESPONSE      analysis.mem_response:156        k / j / - / -
+ *   RTGPU_Q_CPU_RESPONSE      analysis.cpu_response:175        k / j / - / -
+ *   RTGPU_Q_END_TO_END        analysis.end_to_end:191          k / - / - / -
+ *   RTGPU_Q_MEM_WORKLOAD      analysis.mem_workload:109        i / h / t / -
+ *   RTGPU_Q_CPU_WORKLOAD      analysis.cpu_workload:118        i / h / t / -
+ *   RTGPU_Q_R2                end_to_end's R2 recurrence:214   k / - / base / -
+ */
+#define RTGPU_Q_WORKLOAD 0
+#define RTGPU_Q_MAX_WORKLOAD 1
+#define RTGPU_Q_SEGMENT_RESPONSE 2
+#define RTGPU_Q_TASK_RESPONSE 3
+#define RTGPU_Q_MEM_RESPONSE 4
+#define RTGPU_Q_CPU_RESPONSE 5
+#define RTGPU_Q_END_TO_END 6
+#define RTGPU_Q_MEM_WORKLOAD 7
+#define RTGPU_Q_CPU_WORKLOAD 8
+#define RTGPU_Q_R2 9
+
+#define RTGPU_GAP_ERROR 5 /* query status: the reference raises InfeasibleGapError */
+
+typedef struct {
+    int64_t set;      /* index of the set in the batch */
+    int32_t kind;     /* RTGPU_Q_* */
+    int32_t task;     /* task position in the blob (priority order) */
+    int32_t index;    /* start segment h or segment j */
+    int32_t pad;
+    int64_t horizon;  /* window length t (ticks), or the R2 base */
+    int64_t blocking; /* constant blocking term (ticks) */
+} rtgpu_query;
+
+int rtgpu_query_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sets,
+                     const rtgpu_query *queries, int64_t n_queries, int32_t *status,
+                     int64_t *num, int64_t *den);
+
 /* number of kernel launches the last rtgpu_analyze_* call enqueued */
 int64_t rtgpu_last_launch_count(void);
 

@@ -170,8 +170,17 @@ struct VOff {
 template <class V> struct SetCtx {
     typedef typename Num<V>::Qt Qt;
     const i64 *blob; /* global: this set's blob */
-    TaskRec *tr;
-    V *vc, *vm, *scr;
+    /* Shared-memory slab of the warp, as byte offsets from the dynamic
+     * shared-memory base: pointers are rebuilt from the extern __shared__
+     * symbol inside every routine, so the compiler always knows they are
+     * shared (LDS/STS, not generic LD/ST) -- also across out-of-line calls. */
+    unsigned char *hbase; /* host harness only */
+    int o_tr, o_vc, o_vm, o_scr;
+    RT_HD unsigned char *sbase() const;
+    RT_HD TaskRec *TR() const { return (TaskRec *)(sbase() + o_tr); }
+    RT_HD V *VC() const { return (V *)(sbase() + o_vc); }
+    RT_HD V *VM() const { return (V *)(sbase() + o_vm); }
+    RT_HD V *SCR() const { return (V *)(sbase() + o_scr); }
     Layout<V> L;
     int n, GN, mm;
     i64 A;
@@ -189,6 +198,17 @@ template <class V> struct SetCtx {
     i64 evals, budget;
     int budget_hit;
 };
+
+#ifdef __CUDACC__
+extern __shared__ __align__(16) unsigned char rt_dyn_smem[];
+#endif
+template <class V> RT_HD unsigned char *SetCtx<V>::sbase() const {
+#ifdef __CUDA_ARCH__
+    return rt_dyn_smem;
+#else
+    return hbase;
+#endif
+}
 
 /* lane-group sizes (2^lg lanes per hp task) and binary-search first steps */
 template <class V> RT_HD void set_groups(SetCtx<V> &c) {
@@ -323,7 +343,7 @@ struct SeqTeam {
 template <class V>
 RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     typedef Num<V> N;
-    const TaskRec &t = c.tr[i];
+    const TaskRec &t = c.TR()[i];
     const i64 *sg = c.blob + t.seg;
     const int m = t.m, p = t.p, g = m - 1;
     const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
@@ -333,7 +353,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         /* busy-waiting baseline (analysis.py:360): one execution segment of
          * length sum(CL up) + sum(ML up) + sum(GR up), no suspension */
         VOff o(c.MC);
-        V *v = c.vc + (size_t)i * c.L.SC;
+        V *v = c.VC() + (size_t)i * c.L.SC;
         V gru = 0;
         if (t.isgpu) {
             typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * t.g);
@@ -353,7 +373,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     /* CPU chain */
     {
         VOff o(c.MC);
-        V *v = c.vc + (size_t)i * c.L.SC;
+        V *v = c.VC() + (size_t)i * c.L.SC;
         V P = 0, EP = 0;
         for (int j = 0; j < m; j++) {
             V e = N::sc(cl_hi[j], q);
@@ -381,7 +401,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     /* memory chain */
     if (p > 0) {
         VOff o(c.MP);
-        V *v = c.vm + (size_t)i * c.L.SM;
+        V *v = c.VM() + (size_t)i * c.L.SM;
         V P = 0, EP = 0;
         for (int j = 0; j < p; j++) {
             V e = N::sc(ml_hi[j], q);
@@ -509,16 +529,16 @@ template <class V> struct IView {
 template <class V>
 RT_HD IView<V> make_iview(const SetCtx<V> &c, int k, int kind) {
     IView<V> v;
-    v.tr = c.tr;
+    v.tr = c.TR();
     v.k = k;
     v.kind = kind;
     v.lg = kind == K_CPU ? c.lgC : c.lgM;
     v.PM = kind == K_CPU ? c.MC : c.MP;
     v.half = kind == K_CPU ? c.halfC : c.halfM;
     v.stride = kind == K_CPU ? c.L.SC : c.L.SM;
-    v.views = kind == K_CPU ? c.vc : c.vm;
+    v.views = kind == K_CPU ? c.VC() : c.VM();
     v.p1 = c.single_seg;
-    v.prio_k = c.tr[k].prio;
+    v.prio_k = c.TR()[k].prio;
     return v;
 }
 
@@ -620,7 +640,7 @@ RT_HD typename Num<V>::Qt task_scale(SetCtx<V> &c, int k, int g, typename Num<V>
     typedef typename Num<V>::Qt Qt;
     Qt q = lcm_lim<Qt>(lcm_pre, (Qt)1, c.qlim);
     q = (q == 0 || q > c.qlim / 2) ? 0 : q * 2;
-    if (q != 0 && c.tr[k].isgpu) q = lcm_lim<Qt>(q, (Qt)2 * (Qt)c.A * (Qt)g, c.qlim);
+    if (q != 0 && c.TR()[k].isgpu) q = lcm_lim<Qt>(q, (Qt)2 * (Qt)c.A * (Qt)g, c.qlim);
     if (q == 0) c.esc = 1;
     return q;
 }
@@ -629,7 +649,7 @@ RT_HD typename Num<V>::Qt task_scale(SetCtx<V> &c, int k, int g, typename Num<V>
  * sum_j[(gw_hi*an - gl*A)/(2*A*g) + gl] = sInfl*(q/(2Ag)) + sGL*q. */
 template <class V>
 RT_HD V sum_grup(const SetCtx<V> &c, int k, int g, typename Num<V>::Qt q) {
-    const TaskRec &t = c.tr[k];
+    const TaskRec &t = c.TR()[k];
     if (!t.isgpu) return 0;
     typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * g);
     return (V)t.sInfl * (V)per + Num<V>::sc(t.sGL, q);
@@ -646,7 +666,7 @@ template <class V, class TM>
 RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::Qt lcm_pre,
                      bool want_all, TaskEval<V> &res, V *mr_out, V *cr_out) {
     typedef Num<V> N;
-    const TaskRec &t = c.tr[k];
+    const TaskRec &t = c.TR()[k];
     typename N::Qt q = task_scale(c, k, g, lcm_pre);
     res.q = q;
     res.pass = false;
@@ -656,8 +676,8 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
     RT_COUNT(g_cnt_eval);
     ensure_views(tm, c, k, q);
     const V D = N::sc(t.D, q);
-    V *bases = c.scr;
-    V *outs = c.scr + (c.MP + c.MC + 2);
+    V *bases = c.SCR();
+    V *outs = c.SCR() + (c.MP + c.MC + 2);
     const i64 *sg = c.blob + t.seg;
     const i64 *cl_hi = sg + t.m, *ml_hi = sg + 2 * t.m + t.p;
     /* memory segments: analysis.py:156 (blocking = longest lp copy) */
@@ -713,7 +733,7 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
 template <class V>
 RT_NI void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
     const i64 *r = c.blob + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
-    TaskRec &t = c.tr[i];
+    TaskRec &t = c.TR()[i];
     t.m = (int)r[0];
     t.p = (int)r[1];
     t.D = r[2];
@@ -813,14 +833,14 @@ template <class V, class TM>
 RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool stop_at_fail) {
     typedef typename Num<V>::Qt Qt;
     Qt lcm_pre = 1;
-    V *mr = c.scr + 2 * (c.MP + c.MC + 2);
+    V *mr = c.SCR() + 2 * (c.MP + c.MC + 2);
     V *cr = mr + c.MP;
     V *grl = cr + c.MC;
     V *grh = grl + c.MC;
     bool failed = false;
     int k = 0;
     for (; k < c.n; k++) {
-        const TaskRec &t = c.tr[k];
+        const TaskRec &t = c.TR()[k];
         TaskEval<V> res;
         eval_task(tm, c, k, t.g, lcm_pre, true, res, mr, cr);
         if (c.esc || c.stuck) return false;
@@ -900,7 +920,7 @@ RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool sto
             o.den[k] = 1;
         }
         if (o.detail) {
-            const TaskRec &t = c.tr[k];
+            const TaskRec &t = c.TR()[k];
             i64 *d = o.detail + t.seg;
             tm.pfor(2 * t.m + 2 * t.p + 4 * (t.m - 1), [&](int w) { d[w] = RTGPU_ABSENT; });
         }
@@ -913,7 +933,7 @@ RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool sto
 template <class V, class TM>
 RT_HD void set_g(const TM &tm, SetCtx<V> &c, int k, int g) {
     tm.sync();
-    if (tm.leader()) c.tr[k].g = g;
+    if (tm.leader()) c.TR()[k].g = g;
     tm.sync();
     if (c.vn > k) c.vn = k;
 }
@@ -946,9 +966,9 @@ RT_NI int search_greedy(const TM &tm, SetCtx<V> &c) {
     Qt lcm_pre = 1;
     i64 used = 0, rest_min = 0;
     for (int k = 0; k < c.n; k++)
-        if (c.tr[k].isgpu) rest_min += c.tr[k].gmin;
+        if (c.TR()[k].isgpu) rest_min += c.TR()[k].gmin;
     for (int k = 0; k < c.n; k++) {
-        TaskRec &t = c.tr[k];
+        TaskRec &t = c.TR()[k];
         if (!t.isgpu) {
             TaskEval<V> r;
             eval_task(tm, c, k, 0, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
@@ -980,17 +1000,17 @@ RT_NI int search_dfs(const TM &tm, SetCtx<V> &c) {
     for (;;) {
         if (d == c.n) return RTGPU_SCHEDULABLE;
         if (c.budget > 0 && c.evals >= c.budget) return RTGPU_UNDECIDED;
-        TaskRec &t = c.tr[d];
+        TaskRec &t = c.TR()[d];
         Qt lcm_pre = 1;
         i64 used = 0, after = 0;
         for (int i = 0; i < d; i++)
-            if (c.tr[i].isgpu) {
-                lcm_pre = lcm_lim<Qt>(lcm_pre, (Qt)c.tr[i].g, c.qlim);
+            if (c.TR()[i].isgpu) {
+                lcm_pre = lcm_lim<Qt>(lcm_pre, (Qt)c.TR()[i].g, c.qlim);
                 if (lcm_pre == 0) return ST_ESCALATE;
-                used += c.tr[i].g;
+                used += c.TR()[i].g;
             }
         for (int i = d + 1; i < c.n; i++)
-            if (c.tr[i].isgpu) after += c.tr[i].gmin;
+            if (c.TR()[i].isgpu) after += c.TR()[i].gmin;
         bool ok;
         if (!t.isgpu) {
             TaskEval<V> r;
@@ -1013,13 +1033,13 @@ RT_NI int search_dfs(const TM &tm, SetCtx<V> &c) {
         for (;;) {
             d--;
             if (d < 0) return RTGPU_UNSCHEDULABLE;
-            TaskRec &b = c.tr[d];
+            TaskRec &b = c.TR()[d];
             if (!b.isgpu) continue;
             i64 u = 0, a = 0;
             for (int i = 0; i < d; i++)
-                if (c.tr[i].isgpu) u += c.tr[i].g;
+                if (c.TR()[i].isgpu) u += c.TR()[i].g;
             for (int i = d + 1; i < c.n; i++)
-                if (c.tr[i].isgpu) a += c.tr[i].gmin;
+                if (c.TR()[i].isgpu) a += c.TR()[i].gmin;
             if (b.g < c.GN - u - a) {
                 set_g(tm, c, d, b.g + 1);
                 d++;
@@ -1110,7 +1130,7 @@ template <class V> RT_HD bool susp_valid(const SetCtx<V> &c, const TaskRec &t, i
 template <class V, class TM>
 RT_NI V baseline_response(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt q, V B,
                           bool want_all) {
-    const TaskRec &t = c.tr[k];
+    const TaskRec &t = c.TR()[k];
     const V D = Num<V>::sc(t.D, q);
     V sum_sh = 0, sum_eh;
     if (c.single_seg) {
@@ -1122,8 +1142,8 @@ RT_NI V baseline_response(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt
     V r2 = lfp(tm, c, k, K_CPU, sum_sh + sum_eh + B, sum_sh + sum_eh + B, D);
     if (c.single_seg) return r2; /* one segment, no suspension: R1 == R2 */
     if (r2 >= 0 && !want_all) return r2;
-    V *bases = c.scr;
-    V *outs = c.scr + (c.MP + c.MC + 2);
+    V *bases = c.SCR();
+    V *outs = c.SCR() + (c.MP + c.MC + 2);
     const i64 *cl_hi = c.blob + t.seg + t.m;
     tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q) + B; });
     bool none;
@@ -1146,9 +1166,9 @@ template <class V> RT_HD typename Num<V>::Qt alloc_scale(SetCtx<V> &c) {
     Qt L = 1;
     bool any = false;
     for (int i = 0; i < c.n; i++)
-        if (c.tr[i].isgpu) {
+        if (c.TR()[i].isgpu) {
             any = true;
-            L = lcm_lim<Qt>(L, (Qt)c.tr[i].g, c.qlim);
+            L = lcm_lim<Qt>(L, (Qt)c.TR()[i].g, c.qlim);
             if (L == 0) break;
         }
     if (!any) return 1;
@@ -1171,17 +1191,17 @@ RT_NI int eval_alloc_baseline(const TM &tm, SetCtx<V> &c, bool want_all, const O
     c.vn = 0;
     ensure_views(tm, c, c.n, q);
     for (int i = 0; i < c.n; i++)
-        if (!susp_valid(c, c.tr[i], c.tr[i].g, q)) return -1;
+        if (!susp_valid(c, c.TR()[i], c.TR()[i].g, q)) return -1;
     for (int k = 0; k < c.n; k++) {
         c.evals++;
         V B = 0;
         if (c.method == RTGPU_METHOD_SELFSUSP)
             for (int i = 0; i < c.n; i++)
-                if (c.tr[i].prio > c.tr[k].prio) B = tmax(B, max_susp_hi(c, c.tr[i], c.tr[i].g, q));
+                if (c.TR()[i].prio > c.TR()[k].prio) B = tmax(B, max_susp_hi(c, c.TR()[i], c.TR()[i].g, q));
         V r = baseline_response(tm, c, k, q, B, want_all);
         if (c.esc || c.stuck) return -2;
         if (out) {
-            const TaskRec &t = c.tr[k];
+            const TaskRec &t = c.TR()[k];
             tm.sync();
             if (sizeof(V) > 8 && ((i128)q > (i128)INT64_MAX || Num<V>::wide(r) > (i128)INT64_MAX)) {
                 c.esc = 1;
@@ -1212,7 +1232,7 @@ RT_NI int eval_alloc_baseline(const TM &tm, SetCtx<V> &c, bool want_all, const O
 /* smallest count >= lo at which task t is a valid SuspTask (monotone), 0 if none */
 template <class V> RT_HD int min_valid_g(SetCtx<V> &c, int k, int lo) {
     typedef typename Num<V>::Qt Qt;
-    const TaskRec &t = c.tr[k];
+    const TaskRec &t = c.TR()[k];
     for (int g = lo; g <= c.GN; g++) {
         Qt q = (Qt)2 * (Qt)c.A * (Qt)g;
         if (q > c.qlim) {
@@ -1235,8 +1255,8 @@ template <class V, class TM>
 RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
     int ids[RTGPU_MAX_TASKS], lower[RTGPU_MAX_TASKS], nid = 0;
     for (int k = 0; k < c.n; k++)
-        if (c.tr[k].isgpu) {
-            int g = min_valid_g(c, k, c.tr[k].gmin);
+        if (c.TR()[k].isgpu) {
+            int g = min_valid_g(c, k, c.TR()[k].gmin);
             if (c.esc) return ST_ESCALATE;
             if (g == 0) return RTGPU_UNSCHEDULABLE;
             ids[nid] = k;
@@ -1247,7 +1267,7 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
     if (need > c.GN) return RTGPU_UNSCHEDULABLE;
     tm.sync();
     if (tm.leader())
-        for (int q = 0; q < nid; q++) c.tr[ids[q]].g = lower[q];
+        for (int q = 0; q < nid; q++) c.TR()[ids[q]].g = lower[q];
     tm.sync();
     for (;;) {
         if (c.budget > 0 && c.evals >= c.budget) return RTGPU_UNDECIDED;
@@ -1265,8 +1285,8 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
                 if (c.esc) return ST_ESCALATE;
                 V Bmin = 0;
                 for (int i = 0; i < c.n; i++) {
-                    const TaskRec &t = c.tr[i];
-                    if (t.prio <= c.tr[f].prio || !t.isgpu) continue;
+                    const TaskRec &t = c.TR()[i];
+                    if (t.prio <= c.TR()[f].prio || !t.isgpu) continue;
                     const i64 *sg = c.blob + t.seg;
                     const int m = t.m, p = t.p, g = m - 1;
                     const i64 *ml_hi = sg + 2 * m + p, *gl = sg + 2 * m + 2 * p + 2 * g;
@@ -1290,19 +1310,128 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
         int q = pos;
         for (; q >= 0; q--) {
             i64 used = 0, after = 0;
-            for (int a = 0; a < q; a++) used += c.tr[ids[a]].g;
+            for (int a = 0; a < q; a++) used += c.TR()[ids[a]].g;
             for (int a = q + 1; a < nid; a++) after += lower[a];
-            if (c.tr[ids[q]].g + 1 <= c.GN - used - after) break;
+            if (c.TR()[ids[q]].g + 1 <= c.GN - used - after) break;
         }
         if (q < 0) return RTGPU_UNSCHEDULABLE;
         tm.sync();
         if (tm.leader()) {
-            c.tr[ids[q]].g += 1;
-            for (int a = q + 1; a < nid; a++) c.tr[ids[a]].g = lower[a];
+            c.TR()[ids[q]].g += 1;
+            for (int a = q + 1; a < nid; a++) c.TR()[ids[a]].g = lower[a];
         }
         tm.sync();
         c.vn = 0;
     }
+}
+
+/* ------------------------------------------------------------ point queries */
+
+/* One query of include/rtgpu.h rtgpu_query_*: a building block of the
+ * analysis evaluated on a packed set whose kernels carry explicit response
+ * bounds (one physical SM each, alpha = 1, GL = 0, GW = 2 * GR), so every
+ * value lives on the scale q = 2 * A.  Returns a status; *res is the
+ * numerator over q (-1 = None). */
+template <class V, class TM>
+RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 horizon, i64 blocking,
+                    i64 *res_num, i64 *res_den) {
+    typedef typename Num<V>::Qt Qt;
+    const i64 *h = c.blob;
+    c.n = (int)h[0];
+    c.GN = (int)h[1];
+    c.mm = (int)h[2];
+    c.A = h[3];
+    c.vn = 0;
+    c.vq = 0;
+    c.esc = 0;
+    c.stuck = 0;
+    c.evals = 0;
+    c.single_seg = 0;
+    if (c.n < 1 || c.n > c.maxn || c.A < 1 || k < 0 || k >= c.n) return RTGPU_INVALID;
+    i128 vb_max = 0;
+    tm.pfor(c.n, [&](int i) {
+        i128 vb;
+        load_task(c, i, &vb);
+        c.TR()[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
+        c.TR()[i].g = 1;
+    });
+    for (int i = 0; i < c.n; i++) {
+        if (c.TR()[i].flags & TF_UNSUP) return RTGPU_INVALID;
+        vb_max = tmax(vb_max, (i128)c.TR()[i].B);
+    }
+    i128 hz = (i128)(horizon < 0 ? 0 : horizon) + (blocking < 0 ? 0 : blocking);
+    i128 vb = (vb_max + hz) * ((i128)c.n + 2 * RTGPU_MAX_M + 4);
+    if (vb > (i128)Num<V>::limit()) return ST_ESCALATE;
+    c.Vb = (i64)vb;
+    c.qlim = (Qt)(Num<V>::limit() / (Qt)c.Vb);
+    tm.sync();
+    tm.pfor(c.n, [&](int kk) {
+        i64 b = 0;
+        for (int i = 0; i < c.n; i++)
+            if (c.TR()[i].prio > c.TR()[kk].prio) b = tmax(b, c.TR()[i].maxMlu);
+        c.TR()[kk].B = b;
+    });
+    const Qt q = (Qt)2 * (Qt)c.A;
+    if (q > c.qlim) return ST_ESCALATE;
+    ensure_views(tm, c, c.n, q);
+    const TaskRec &t = c.TR()[k];
+    const i64 *sg = c.blob + t.seg;
+    const V D = Num<V>::sc(t.D, q);
+    V r = (V)-1;
+    *res_den = (i64)q;
+    if (kind == RTGPU_Q_WORKLOAD || kind == RTGPU_Q_MAX_WORKLOAD || kind == RTGPU_Q_CPU_WORKLOAD ||
+        kind == RTGPU_Q_MEM_WORKLOAD) {
+        const bool mem = kind == RTGPU_Q_MEM_WORKLOAD;
+        const int p = mem ? t.p : t.m;
+        if (p == 0) {
+            *res_num = 0;
+            return RTGPU_SCHEDULABLE;
+        }
+        const int PM = mem ? c.MP : c.MC;
+        const V *view = (mem ? c.VM() + (size_t)k * c.L.SM : c.VC() + (size_t)k * c.L.SC);
+        const int half = mem ? c.halfM : c.halfC;
+        const V H = Num<V>::sc(horizon, q);
+        V best = 0;
+        bool err = false;
+        const int h0 = kind == RTGPU_Q_MAX_WORKLOAD ? 0 : idx;
+        const int h1 = kind == RTGPU_Q_MAX_WORKLOAD ? p : idx + 1;
+        if (h0 < 0 || h1 > p) return RTGPU_INVALID;
+        for (int hh = h0; hh < h1; hh++) {
+            V rho;
+            V w = walk(view, PM, half, p, hh, H, rho, err);
+            if (hh == h0 || w > best) best = w;
+        }
+        if (err) return RTGPU_GAP_ERROR;
+        r = best;
+    } else if (kind == RTGPU_Q_SEGMENT_RESPONSE) {
+        if (idx < 0 || idx >= t.m) return RTGPU_INVALID;
+        V b = Num<V>::sc(sg[t.m + idx] + blocking, q);
+        r = lfp(tm, c, k, K_CPU, b, b, D);
+    } else if (kind == RTGPU_Q_TASK_RESPONSE) {
+        r = baseline_response(tm, c, k, q, Num<V>::sc(blocking, q), true);
+    } else if (kind == RTGPU_Q_MEM_RESPONSE) {
+        if (idx < 0 || idx >= t.p) return RTGPU_INVALID;
+        V b = Num<V>::sc(sg[2 * t.m + t.p + idx] + t.B, q);
+        r = lfp(tm, c, k, K_MEM, b, b, D);
+    } else if (kind == RTGPU_Q_CPU_RESPONSE) {
+        if (idx < 0 || idx >= t.m) return RTGPU_INVALID;
+        V b = Num<V>::sc(sg[t.m + idx], q);
+        r = lfp(tm, c, k, K_CPU, b, b, D);
+    } else if (kind == RTGPU_Q_END_TO_END) {
+        TaskEval<V> res;
+        eval_task(tm, c, k, 1, (Qt)1, true, res, (V *)nullptr, (V *)nullptr);
+        r = res.e2e;
+    } else if (kind == RTGPU_Q_R2) {
+        V b = Num<V>::sc(horizon, q);
+        r = lfp(tm, c, k, K_CPU, b, b, D);
+    } else {
+        return RTGPU_INVALID;
+    }
+    if (c.esc) return ST_ESCALATE;
+    if (c.stuck) return RTGPU_UNDECIDED;
+    if (sizeof(V) > 8 && Num<V>::wide(r) > (i128)INT64_MAX) return ST_ESCALATE;
+    *res_num = r < 0 ? (i64)RTGPU_NONE : (i64)Num<V>::wide(r);
+    return RTGPU_SCHEDULABLE;
 }
 
 /* Whole pipeline for one set; returns the status (or ST_ESCALATE). */
@@ -1335,22 +1464,22 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
             i128 vb;
             load_task(c, i, &vb);
             /* store the clamped bound temporarily in B (recomputed below) */
-            c.tr[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
+            c.TR()[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
         });
-        for (int i = 0; i < c.n; i++) vb_max = tmax(vb_max, (i128)c.tr[i].B);
+        for (int i = 0; i < c.n; i++) vb_max = tmax(vb_max, (i128)c.TR()[i].B);
     }
     for (int k = 0; k < c.n; k++)
-        if (c.tr[k].flags & TF_UNSUP) return RTGPU_INVALID;
+        if (c.TR()[k].flags & TF_UNSUP) return RTGPU_INVALID;
     /* reference order: the first task whose min-SM search raises or fails */
     for (int k = 0; k < c.n; k++) {
-        if (c.tr[k].flags & TF_INV) return RTGPU_INVALID;
-        if (c.tr[k].flags & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE;
+        if (c.TR()[k].flags & TF_INV) return RTGPU_INVALID;
+        if (c.TR()[k].flags & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE;
     }
     i64 need = 0;
     bool irregular = false;
     for (int k = 0; k < c.n; k++) {
-        if (c.tr[k].isgpu) need += c.tr[k].gmin;
-        if (c.tr[k].flags & TF_IRREG) irregular = true;
+        if (c.TR()[k].isgpu) need += c.TR()[k].gmin;
+        if (c.TR()[k].flags & TF_IRREG) irregular = true;
     }
     if (need > c.GN) return RTGPU_UNSCHEDULABLE;
     i128 factor = (i128)c.n + 2 * RTGPU_MAX_M + 4;
@@ -1363,14 +1492,14 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
     tm.pfor(c.n, [&](int k) {
         i64 b = 0;
         for (int i = 0; i < c.n; i++)
-            if (c.tr[i].prio > c.tr[k].prio) b = tmax(b, c.tr[i].maxMlu);
-        c.tr[k].B = b;
+            if (c.TR()[i].prio > c.TR()[k].prio) b = tmax(b, c.TR()[i].maxMlu);
+        c.TR()[k].B = b;
     });
     const bool rtg = c.method == RTGPU_METHOD_RTGPU;
     int st = !rtg ? search_baseline(tm, c) : irregular ? search_dfs(tm, c) : search_greedy(tm, c);
     if (st == ST_ESCALATE) return st;
     if (st == RTGPU_SCHEDULABLE) {
-        tm.pfor(c.n, [&](int i) { o.vsm[i] = c.tr[i].isgpu ? 2 * c.tr[i].g : 0; });
+        tm.pfor(c.n, [&](int i) { o.vsm[i] = c.TR()[i].isgpu ? 2 * c.TR()[i].g : 0; });
     }
     if ((flags & (RTGPU_F_BOUNDS | RTGPU_F_DETAIL)) &&
         (st == RTGPU_SCHEDULABLE || st == RTGPU_UNSCHEDULABLE)) {
@@ -1380,14 +1509,14 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
             int first = -1;
             i64 others = 0;
             for (int k = 0; k < c.n; k++)
-                if (c.tr[k].isgpu) {
+                if (c.TR()[k].isgpu) {
                     if (first < 0) first = k;
-                    else others += c.tr[k].gmin;
+                    else others += c.TR()[k].gmin;
                 }
             tm.sync();
             if (tm.leader())
                 for (int k = 0; k < c.n; k++)
-                    c.tr[k].g = c.tr[k].isgpu ? (k == first ? (int)(c.GN - others) : c.tr[k].gmin) : 0;
+                    c.TR()[k].g = c.TR()[k].isgpu ? (k == first ? (int)(c.GN - others) : c.TR()[k].gmin) : 0;
             tm.sync();
             c.vn = 0;
         }

@@ -36,17 +36,16 @@ template <> struct MinBlocks<i128> { static constexpr int value = 2; };
 
 template <class V>
 __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KParams p, int stage) {
-    extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     Layout<V> L;
     L.init(p.dims);
-    unsigned char *slab = smem + (size_t)warp * L.bytes;
     SetCtx<V> c;
-    c.tr = (TaskRec *)slab;
-    c.vc = (V *)(slab + L.off_views_c);
-    c.vm = (V *)(slab + L.off_views_m);
-    c.scr = (V *)(slab + L.off_scr);
+    c.hbase = nullptr;
+    c.o_tr = warp * L.bytes;
+    c.o_vc = c.o_tr + L.off_views_c;
+    c.o_vm = c.o_tr + L.off_views_m;
+    c.o_scr = c.o_tr + L.off_scr;
     c.L = L;
     c.maxn = p.dims.maxn;
     c.MC = p.dims.MC;
@@ -92,6 +91,73 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
     }
 }
 
+
+/* ------------------------------------------------------------ point queries */
+
+struct QParams {
+    const i64 *blobs, *set_off;
+    const rtgpu_query *queries;
+    i64 n;
+    Dims dims;
+    int32_t *status;
+    i64 *num, *den;
+    unsigned long long *ctr;
+    i64 *esc0, *esc1;
+};
+
+template <class V>
+__global__ void __launch_bounds__(256, MinBlocks<V>::value) query_kernel(QParams p, int stage) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    Layout<V> L;
+    L.init(p.dims);
+    SetCtx<V> c;
+    c.hbase = nullptr;
+    c.o_tr = warp * L.bytes;
+    c.o_vc = c.o_tr + L.off_views_c;
+    c.o_vm = c.o_tr + L.off_views_m;
+    c.o_scr = c.o_tr + L.off_scr;
+    c.L = L;
+    c.maxn = p.dims.maxn;
+    c.MC = p.dims.MC;
+    c.MP = p.dims.MP;
+    set_groups(c);
+    c.budget = 0;
+    c.method = RTGPU_METHOD_RTGPU;
+    WarpTeam tm{lane};
+    const i64 count = stage == 0 ? p.n : (i64)(stage == 1 ? p.ctr[3] : p.ctr[4]);
+    const i64 *list = stage == 0 ? nullptr : (stage == 1 ? p.esc0 : p.esc1);
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(&p.ctr[stage], 1ull);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if ((i64)idx >= count) break;
+        const i64 qi = list ? list[idx] : (i64)idx;
+        const rtgpu_query qq = p.queries[qi];
+        c.blob = p.blobs + p.set_off[qq.set];
+        i64 num = RTGPU_NONE, den = 1;
+        int st = run_query(tm, c, qq.kind, qq.task, qq.index, qq.horizon, qq.blocking, &num, &den);
+        if (st == ST_ESCALATE) {
+            if (stage < 2) {
+                if (lane == 0) {
+                    unsigned long long pos = atomicAdd(&p.ctr[3 + stage], 1ull);
+                    (stage == 0 ? p.esc0 : p.esc1)[pos] = qi;
+                }
+                __syncwarp();
+                continue;
+            }
+            st = RTGPU_RANGE;
+        }
+        if (lane == 0) {
+            p.status[qi] = st;
+            p.num[qi] = num;
+            p.den[qi] = den;
+        }
+        __syncwarp();
+    }
+}
+
+template <class V> inline int launch_query_stage(const QParams &p, int stage, cudaStream_t st);
 
 void set_err(const char *what, cudaError_t e);
 void set_err_msg(const char *msg);
@@ -144,6 +210,34 @@ template <class V> inline int launch_stage(const KParams &p, int stage, cudaStre
 }
 
 
+template <class V> inline int launch_query_stage(const QParams &p, int stage, cudaStream_t st) {
+    int bytes = 0;
+    int wpb = warps_per_block<V>(p.dims, &bytes);
+    if (wpb == 0) {
+        set_err_msg("task sets too large for shared memory");
+        return -3;
+    }
+    cudaError_t e = cudaFuncSetAttribute(query_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) {
+        set_err("cudaFuncSetAttribute", e);
+        return -4;
+    }
+    i64 grid = stage == 0 ? (p.n + wpb - 1) / wpb : 148;
+    if (grid > 148 * 8) grid = 148 * 8;
+    if (grid < 1) grid = 1;
+    query_kernel<V><<<(unsigned)grid, 32 * wpb, bytes, st>>>(p, stage);
+    count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_err("query_kernel launch", e);
+        return -5;
+    }
+    return 0;
+}
+
+int launch_query_f64(const QParams &p, int stage, cudaStream_t st);
+int launch_query_i64(const QParams &p, int stage, cudaStream_t st);
+int launch_query_i128(const QParams &p, int stage, cudaStream_t st);
 int launch_stage_f64(const KParams &p, int stage, cudaStream_t st);
 int launch_stage_i64(const KParams &p, int stage, cudaStream_t st);
 int launch_stage_i128(const KParams &p, int stage, cudaStream_t st);

@@ -208,6 +208,56 @@ int rtgpu_analyze_device(const int64_t *d_blobs, const int64_t *d_set_off,
                       (i64 *)d_e2e_num, (i64 *)d_den, (i64 *)d_detail, (cudaStream_t)stream);
 }
 
+int rtgpu_query_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sets,
+                     const rtgpu_query *queries, int64_t n_queries, int32_t *status, int64_t *num,
+                     int64_t *den) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_launches = 0;
+    if (n_queries <= 0) return 0;
+    Dims d;
+    scan_dims_host((const i64 *)blobs, (const i64 *)set_off, n_sets, &d);
+    const size_t W = (size_t)set_off[n_sets];
+    DevBuf b_blob, b_off, b_q, b_st, b_num, b_den, b_scr;
+    if (!b_blob.ensure(W * 8) || !b_off.ensure((n_sets + 1) * 8) ||
+        !b_q.ensure(n_queries * sizeof(rtgpu_query)) || !b_st.ensure(n_queries * 4) ||
+        !b_num.ensure(n_queries * 8) || !b_den.ensure(n_queries * 8) ||
+        !b_scr.ensure(8 * sizeof(unsigned long long) + 2 * 8 * (size_t)n_queries)) {
+        set_err("cudaMalloc", cudaGetLastError());
+        return -6;
+    }
+    cudaStream_t st = 0;
+    cudaMemcpyAsync(b_blob.p, blobs, W * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(b_off.p, set_off, (n_sets + 1) * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(b_q.p, queries, n_queries * sizeof(rtgpu_query), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(b_scr.p, 0, 8 * sizeof(unsigned long long), st);
+    QParams p;
+    p.blobs = (const i64 *)b_blob.p;
+    p.set_off = (const i64 *)b_off.p;
+    p.queries = (const rtgpu_query *)b_q.p;
+    p.n = n_queries;
+    p.dims = d;
+    p.status = (int32_t *)b_st.p;
+    p.num = (i64 *)b_num.p;
+    p.den = (i64 *)b_den.p;
+    p.ctr = (unsigned long long *)b_scr.p;
+    p.esc0 = (i64 *)((char *)b_scr.p + 8 * sizeof(unsigned long long));
+    p.esc1 = p.esc0 + n_queries;
+    int rc = launch_query_f64(p, 0, st);
+    if (!rc) rc = launch_query_i64(p, 1, st);
+    if (!rc) rc = launch_query_i128(p, 2, st);
+    if (rc) return rc;
+    cudaMemcpyAsync(status, b_st.p, n_queries * 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(num, b_num.p, n_queries * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(den, b_den.p, n_queries * 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    for (DevBuf *b : {&b_blob, &b_off, &b_q, &b_st, &b_num, &b_den, &b_scr}) cudaFree(b->p);
+    if (e != cudaSuccess) {
+        set_err("rtgpu_query_host", e);
+        return -8;
+    }
+    return 0;
+}
+
 int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64_t *task_base,
                        int64_t n_sets, int method, unsigned flags, int64_t eval_budget,
                        int32_t *status, int64_t *evals, int32_t *vsm, int64_t *e2e_num,

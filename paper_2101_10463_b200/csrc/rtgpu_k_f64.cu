@@ -3,4 +3,5 @@
 
 namespace rtgpu {
 int launch_stage_f64(const KParams &p, int stage, cudaStream_t st) { return launch_stage<double>(p, stage, st); }
+int launch_query_f64(const QParams &p, int stage, cudaStream_t st) { return launch_query_stage<double>(p, stage, st); }
 }  // namespace rtgpu

@@ -107,6 +107,31 @@ def _check_shape(ts: TaskSet) -> None:
             raise ValueError(f"task {t.id}: mem segment count != {want}")
 
 
+def build_blob(rows: Sequence[dict], physical_sms: int, mem_model_code: int, alpha_den: int) -> list[int]:
+    """Blob from integer task rows (keys: m, p, D, T, prio, idx, cl_lo, cl_hi,
+    ml_lo, ml_hi, gw_lo, gw_hi, gl, an), already in priority order."""
+    n = len(rows)
+    header = [n, physical_sms, mem_model_code, alpha_den, 0,
+              max((r["m"] for r in rows), default=0), max((r["p"] for r in rows), default=0), 0]
+    records: list[int] = []
+    segs: list[int] = []
+    base = HDR_WORDS + TASK_WORDS * n
+    for r in rows:
+        records += [r["m"], r["p"], r["D"], r["T"], r["prio"], base + len(segs), r["idx"], 0]
+        for key in ("cl_lo", "cl_hi", "ml_lo", "ml_hi", "gw_lo", "gw_hi", "gl", "an"):
+            segs += list(r[key])
+    blob = header + records + segs
+    blob[4] = len(blob)
+    for v in blob:
+        if not -INT64_MAX <= v <= INT64_MAX:
+            raise EngineRangeError("task set values exceed int64 after scaling")
+    return blob
+
+
+def lcm_denominators(values) -> int:
+    return _lcm_all(Fraction(v).denominator for v in values)
+
+
 def pack_set(ts: TaskSet) -> tuple[list[int], int, tuple]:
     """One blob as a list of Python ints plus its time scale and task order."""
     _check_shape(ts)

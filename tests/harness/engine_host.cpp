@@ -27,10 +27,11 @@ int run_one(const Dims &d, const i64 *blob, int method, unsigned flags, i64 budg
     unsigned char *base = (unsigned char *)(((uintptr_t)slab.data() + 15) & ~(uintptr_t)15);
     SetCtx<V> c;
     c.blob = blob;
-    c.tr = (TaskRec *)base;
-    c.vc = (V *)(base + L.off_views_c);
-    c.vm = (V *)(base + L.off_views_m);
-    c.scr = (V *)(base + L.off_scr);
+    c.hbase = base;
+    c.o_tr = 0;
+    c.o_vc = L.off_views_c;
+    c.o_vm = L.off_views_m;
+    c.o_scr = L.off_scr;
     c.L = L;
     c.maxn = d.maxn;
     c.MC = d.MC;
@@ -86,6 +87,60 @@ extern "C" int host_analyze_batch(const int64_t *blobs, const int64_t *set_off,
         if (st == ST_ESCALATE) st = RTGPU_RANGE;
         status[s] = st;
         if (stage_used) stage_used[s] = stage - 1;
+    }
+    return 0;
+}
+
+extern "C" int host_query(const int64_t *blobs, const int64_t *set_off, int64_t n_sets,
+                          const rtgpu_query *qs, int64_t nq, int32_t *status, int64_t *num,
+                          int64_t *den) {
+    Dims d;
+    d.maxn = 1;
+    d.MC = 1;
+    d.MP = 0;
+    for (int64_t s = 0; s < n_sets; s++) {
+        const int64_t *h = blobs + set_off[s];
+        if (h[0] > d.maxn) d.maxn = (int)h[0];
+        if (h[5] > d.MC) d.MC = (int)h[5];
+        if (h[6] > d.MP) d.MP = (int)h[6];
+    }
+    for (int64_t qi = 0; qi < nq; qi++) {
+        const rtgpu_query &q = qs[qi];
+        int st = ST_ESCALATE;
+        for (int stage = 0; stage < 3 && st == ST_ESCALATE; stage++) {
+            auto go = [&](auto tag) {
+                typedef decltype(tag) V;
+                Layout<V> L;
+                L.init(d);
+                std::vector<unsigned char> slab((size_t)L.bytes + 64);
+                unsigned char *base = (unsigned char *)(((uintptr_t)slab.data() + 15) & ~(uintptr_t)15);
+                SetCtx<V> c;
+                c.blob = (const i64 *)blobs + set_off[q.set];
+                c.hbase = base;
+                c.o_tr = 0;
+                c.o_vc = L.off_views_c;
+                c.o_vm = L.off_views_m;
+                c.o_scr = L.off_scr;
+                c.L = L;
+                c.maxn = d.maxn;
+                c.MC = d.MC;
+                c.MP = d.MP;
+                set_groups(c);
+                c.budget = 0;
+                c.method = 0;
+                SeqTeam tm;
+                i64 n = RTGPU_NONE, dd = 1;
+                int r = run_query(tm, c, q.kind, q.task, q.index, q.horizon, q.blocking, &n, &dd);
+                num[qi] = n;
+                den[qi] = dd;
+                return r;
+            };
+            if (stage == 0) st = go(0.0);
+            else if (stage == 1) st = go((i64)0);
+            else st = go((i128)0);
+        }
+        if (st == ST_ESCALATE) st = RTGPU_RANGE;
+        status[qi] = st;
     }
     return 0;
 }

@@ -57,3 +57,28 @@ def analyze_batch(blobs, set_off, task_base, flags=2, budget=0, first_stage=0, d
         _p(out["den"], ctypes.c_int64), _p(out["detail"], ctypes.c_int64),
         _p(out["stage"], ctypes.c_int32))
     return out
+
+
+def query(sets, queries):
+    """host_query over blobs (int lists) and (set, kind, task, index, horizon,
+    blocking) tuples; returns (status, num, den) per query."""
+    from paper_2101_10463_b200.queries import QueryC
+    L = lib()
+    words, offs = [], [0]
+    for b in sets:
+        words += b
+        offs.append(len(words))
+    blobs = np.asarray(words, dtype=np.int64)
+    set_off = np.asarray(offs, dtype=np.int64)
+    n = len(queries)
+    qa = (QueryC * n)(*[QueryC(s, k, t, i, 0, h, b) for s, k, t, i, h, b in queries])
+    st = np.zeros(n, np.int32)
+    num = np.zeros(n, np.int64)
+    den = np.ones(n, np.int64)
+    L.host_query.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                             ctypes.c_int64, ctypes.POINTER(QueryC), ctypes.c_int64,
+                             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
+                             ctypes.POINTER(ctypes.c_int64)]
+    L.host_query(_p(blobs, ctypes.c_int64), _p(set_off, ctypes.c_int64), len(sets), qa, n,
+                 _p(st, ctypes.c_int32), _p(num, ctypes.c_int64), _p(den, ctypes.c_int64))
+    return [(int(st[i]), int(num[i]), int(den[i])) for i in range(n)]
