@@ -1,0 +1,64 @@
+/*
+ * rtgpu_exec.h -- C-ABI of the SM-partitioned persistent-thread executor
+ * (csrc/executor.cu): the paper's accelerator mechanism (RTGPU section 4,
+ * Algorithm 1) on the GPU, whose measured response times are checked against
+ * the analysis (the reference checks its discrete-event simulator the same
+ * way: simulator.py check_against_analysis).
+ */
+#ifndef RTGPU_EXEC_H
+#define RTGPU_EXEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTGPU_EXEC_MASK_WORDS 8    /* SM bitmap: up to 256 SMs            */
+#define RTGPU_EXEC_BLOCKS_PER_SM 6 /* launch width per SM (>= 2 slots)    */
+
+typedef struct {
+    int32_t m;                    /* CPU segments                              */
+    int32_t two_copy;             /* 1: H2D before and D2H after each kernel   */
+    int32_t n_copies;             /* memory copies (2m-2 or m-1)               */
+    int32_t slots_per_sm;         /* virtual SMs per physical SM (2)           */
+    int64_t cpu_us[16];           /* CPU segment lengths (host busy wait)      */
+    int64_t copy_bytes[30];       /* bytes of each copy                        */
+    int64_t kernel_items[15];     /* work items of each kernel                 */
+    int32_t kernel_iters;         /* FMA iterations per item                   */
+    int32_t priority;
+    uint32_t sm_mask[RTGPU_EXEC_MASK_WORDS]; /* the task's physical SMs        */
+    int64_t period_us;
+    int64_t deadline_us;
+} rtgpu_exec_task;
+
+typedef struct {
+    int64_t jobs;
+    int64_t deadline_misses;
+    double max_response_us;       /* measured worst-case response time        */
+    double mean_response_us;
+    double max_kernel_us;         /* worst kernel time (CUDA events)          */
+    double max_kernel_wall_us;    /* worst kernel time incl. launch (host)    */
+    double max_copy_us;
+} rtgpu_exec_result;
+
+const char *rtgpu_exec_last_error(void);
+
+/* Time `reps` launches of one persistent segment on partition `mask` with
+ * `nslots` blocks per SM; blocks_out = participating blocks of the first
+ * launch (-1 if any ran outside the mask), sms_out = distinct SMs used. */
+int rtgpu_exec_kernel_ms(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
+                         float *ms_out, int32_t *blocks_out, int32_t *sms_out);
+
+/* Time `reps` pinned-host copies of `bytes` (to_device: H2D, else D2H). */
+int rtgpu_exec_copy_ms(int64_t bytes, int to_device, int reps, float *ms_out);
+
+/* Run the task set for horizon_us with periodic releases; per-task results. */
+int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
+                   rtgpu_exec_result *results);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

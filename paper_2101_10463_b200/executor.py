@@ -1,0 +1,251 @@
+"""SM-partitioned persistent-thread executor (include/rtgpu_exec.h) and the
+measured-WCRT-vs-bound experiment (BASELINE config 4).
+
+Pipeline:
+  1. calibrate the GPU timing model on the device: single-SM time of each
+     kernel (GW), the two-slot interleave ratio (alpha = 2 t2 / t1, section
+     4.3), the launch / critical-path overhead (GL) and copy times (ML);
+  2. build the task set in the analysis' model from those measurements
+     (upper bounds rounded up with a safety margin) and run analyze_rtgpu on
+     the GPU engine to get an SM allocation and the bounds R_k;
+  3. pin each task's kernels to its disjoint SM partition and run the tasks
+     concurrently with periodic releases, measuring every job's response;
+  4. check measured WCRT <= R_k and measured kernel times <= GR_up.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+from .analysis import analyze_rtgpu
+from .gpu import gpu_response_bounds
+from .model import ExecBounds, GpuKernelModel, MemModel, PlatformConfig, TaskSet, TaskSpec
+
+MASK_WORDS = 8
+
+
+class ExecTaskC(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("two_copy", ctypes.c_int32),
+                ("n_copies", ctypes.c_int32), ("slots_per_sm", ctypes.c_int32),
+                ("cpu_us", ctypes.c_int64 * 16), ("copy_bytes", ctypes.c_int64 * 30),
+                ("kernel_items", ctypes.c_int64 * 15), ("kernel_iters", ctypes.c_int32),
+                ("priority", ctypes.c_int32), ("sm_mask", ctypes.c_uint32 * MASK_WORDS),
+                ("period_us", ctypes.c_int64), ("deadline_us", ctypes.c_int64)]
+
+
+class ExecResultC(ctypes.Structure):
+    _fields_ = [("jobs", ctypes.c_int64), ("deadline_misses", ctypes.c_int64),
+                ("max_response_us", ctypes.c_double), ("mean_response_us", ctypes.c_double),
+                ("max_kernel_us", ctypes.c_double), ("max_kernel_wall_us", ctypes.c_double),
+                ("max_copy_us", ctypes.c_double)]
+
+
+def _lib():
+    L = _native.lib()
+    if not getattr(L, "_exec_ready", False):
+        L.rtgpu_exec_kernel_ms.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_int,
+                                           ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_float),
+                                           ctypes.POINTER(ctypes.c_int32),
+                                           ctypes.POINTER(ctypes.c_int32)]
+        L.rtgpu_exec_copy_ms.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_float)]
+        L.rtgpu_exec_run.argtypes = [ctypes.POINTER(ExecTaskC), ctypes.c_int, ctypes.c_double,
+                                     ctypes.POINTER(ExecResultC)]
+        L.rtgpu_exec_last_error.restype = ctypes.c_char_p
+        L._exec_ready = True
+    return L
+
+
+def mask_of(sms) -> "ctypes.Array":
+    m = (ctypes.c_uint32 * MASK_WORDS)()
+    for s in sms:
+        m[s >> 5] |= 1 << (s & 31)
+    return m
+
+
+def kernel_ms(sms, nslots: int, items: int, iters: int, reps: int = 5):
+    """Times (ms) of `reps` launches on the SM list; also participating blocks
+    of the first launch (-1 if a block ran outside the partition) and the
+    number of distinct SMs that ran it."""
+    _native.require_device()
+    out = (ctypes.c_float * reps)()
+    nb, ns = ctypes.c_int32(0), ctypes.c_int32(0)
+    rc = _lib().rtgpu_exec_kernel_ms(mask_of(sms), nslots, items, iters, reps, out,
+                                     ctypes.byref(nb), ctypes.byref(ns))
+    if rc:
+        raise RuntimeError(_lib().rtgpu_exec_last_error().decode())
+    return [float(x) for x in out], nb.value, ns.value
+
+
+def copy_ms(nbytes: int, to_device: bool, reps: int = 5):
+    out = (ctypes.c_float * reps)()
+    if _lib().rtgpu_exec_copy_ms(nbytes, 1 if to_device else 0, reps, out):
+        raise RuntimeError(_lib().rtgpu_exec_last_error().decode())
+    return [float(x) for x in out]
+
+
+@dataclass
+class KernelCal:
+    items: int
+    iters: int
+    t1_us: float      # one SM, one slot (the paper's single-SM time GW)
+    t2_us: float      # one SM, two slots
+    alpha: Fraction   # 2 t2 / t1, rounded up to a percent
+    lo_us: int
+    hi_us: int
+
+
+@dataclass
+class ExecTaskDef:
+    cpu_us: list
+    copy_bytes: list
+    kernel_items: list
+    period_us: int = 0
+    deadline_us: int = 0
+
+
+@dataclass
+class WcrtReport:
+    tasks: list = field(default_factory=list)
+    allocation: dict = field(default_factory=dict)
+    schedulable: bool = False
+    all_within_bound: bool = False
+    kernels_within_bound: bool = False
+    max_ratio: float = 0.0
+    horizon_us: float = 0.0
+    note: str = ""
+
+
+def _ceil_margin(x_us: float, margin: float) -> int:
+    return int(math.ceil(x_us * (1 + margin))) + 1
+
+
+def calibrate_kernel(items: int, iters: int, reps: int = 5, margin: float = 0.08,
+                     sm: int = 0) -> KernelCal:
+    t1 = kernel_ms([sm], 1, items, iters, reps)[0]
+    t2 = kernel_ms([sm], 2, items, iters, reps)[0]
+    t1u, t2u = max(t1) * 1e3, max(t2) * 1e3
+    alpha = Fraction(max(100, min(180, math.ceil(200 * t2u / t1u))), 100)
+    return KernelCal(items, iters, t1u, t2u, alpha, int(min(t1) * 1e3 * 0.95),
+                     _ceil_margin(t1u, margin))
+
+
+def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = True):
+    L = _lib()
+    n = len(defs)
+    arr = (ExecTaskC * n)()
+    for i, (d, sms) in enumerate(zip(defs, partitions)):
+        t = arr[i]
+        t.m = len(d.cpu_us)
+        t.two_copy = 1 if two_copy else 0
+        t.n_copies = len(d.copy_bytes)
+        t.slots_per_sm = 2
+        for j, v in enumerate(d.cpu_us):
+            t.cpu_us[j] = int(v)
+        for j, v in enumerate(d.copy_bytes):
+            t.copy_bytes[j] = int(v)
+        for j, v in enumerate(d.kernel_items):
+            t.kernel_items[j] = int(v)
+        t.kernel_iters = iters
+        t.priority = i + 1
+        mk = mask_of(sms)
+        for w in range(MASK_WORDS):
+            t.sm_mask[w] = mk[w]
+        t.period_us = int(d.period_us)
+        t.deadline_us = int(d.deadline_us)
+    res = (ExecResultC * n)()
+    if L.rtgpu_exec_run(arr, n, float(horizon_us), res):
+        raise RuntimeError(L.rtgpu_exec_last_error().decode())
+    return [res[i] for i in range(n)]
+
+
+def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int = 0,
+                    utilization: float = 0.45, horizon_us: float = 3e6, n_sm: int = 148,
+                    margin: float = 0.08) -> WcrtReport:
+    """BASELINE config 4: n concurrent tasks on disjoint SM partitions of the
+    GPU; measured WCRT vs the RTGPU bound R_k."""
+    _native.require_device()
+    rng = np.random.default_rng(seed)
+    defs = []
+    for i in range(n_tasks):
+        defs.append(ExecTaskDef(
+            cpu_us=[int(x) for x in rng.integers(100, 600, m)],
+            copy_bytes=[int(x) for x in rng.integers(1 << 18, 4 << 20, 2 * m - 2)],
+            kernel_items=[int(x) for x in rng.integers(400, 3000, m - 1)]))
+    # calibrate every kernel and copy on the device
+    cal = {}
+    for d in defs:
+        for it in d.kernel_items:
+            if it not in cal:
+                cal[it] = calibrate_kernel(it, iters, margin=margin)
+    overhead = max(kernel_ms(list(range(8)), 2, 0, iters, 5)[0]) * 1e3
+    GL = _ceil_margin(overhead, margin)
+    copy_cal = {}
+    for d in defs:
+        for j, b in enumerate(d.copy_bytes):
+            key = (b, j % 2 == 0)
+            if key not in copy_cal:
+                ts = copy_ms(b, j % 2 == 0, 5)
+                copy_cal[key] = (int(min(ts) * 1e3 * 0.9), _ceil_margin(max(ts) * 1e3, margin + 0.5))
+    # the analysis' task set (integer microseconds; upper bounds padded)
+    specs = []
+    util = rng.uniform(0.5, 1.5, n_tasks)
+    util = util / util.sum() * utilization
+    for i, d in enumerate(defs):
+        cpu = tuple(ExecBounds.exact(c) for c in d.cpu_us)
+        mem = tuple(ExecBounds(Fraction(copy_cal[(b, j % 2 == 0)][0]),
+                               Fraction(copy_cal[(b, j % 2 == 0)][1]))
+                    for j, b in enumerate(d.copy_bytes))
+        gpu = tuple(GpuKernelModel(ExecBounds(Fraction(min(cal[it].lo_us, cal[it].hi_us)),
+                                              Fraction(cal[it].hi_us)),
+                                   Fraction(min(GL, cal[it].lo_us)), cal[it].alpha)
+                    for it in d.kernel_items)
+        demand = sum(c.hi for c in cpu) + sum(x.hi for x in mem) + sum(g.work.hi for g in gpu)
+        D = int(demand / Fraction(util[i]).limit_denominator(10**6))
+        d.period_us = d.deadline_us = D
+        specs.append(TaskSpec(f"x{i}", cpu, mem, gpu, Fraction(D), Fraction(D), 0))
+    order = sorted(range(n_tasks), key=lambda i: (specs[i].deadline, i))
+    specs = [TaskSpec(s.id, s.cpu_segments, s.mem_segments, s.gpu_segments, s.deadline, s.period,
+                      order.index(i) + 1) for i, s in enumerate(specs)]
+    ts = TaskSet(tuple(specs), MemModel.TWO_COPY, PlatformConfig(n_sm, Fraction(3, 25)))
+    report = analyze_rtgpu(ts)
+    out = WcrtReport(schedulable=report.schedulable, horizon_us=horizon_us)
+    if not report.schedulable:
+        out.note = "analysis rejects the calibrated task set; nothing to execute"
+        return out
+    # disjoint partitions: consecutive SM ids in priority order
+    alloc = report.allocation.per_task_virtual_sms
+    parts, nxt = [], 0
+    for s in specs:
+        gn = alloc[s.id] // 2
+        parts.append(list(range(nxt, nxt + gn)))
+        nxt += gn
+    out.allocation = {s.id: alloc[s.id] for s in specs}
+    res = run_tasks(defs, parts, iters, horizon_us)
+    ratios, kok = [], True
+    for s, d, r, sms in zip(specs, defs, res, parts):
+        bound = report.per_task[s.id].end_to_end_up
+        grs = [gpu_response_bounds(g, 2 * len(sms)).hi for g in s.gpu_segments]
+        ratio = r.max_response_us / float(bound)
+        ratios.append(ratio)
+        kern_ok = r.max_kernel_us <= float(max(grs))
+        kok = kok and kern_ok
+        out.tasks.append({"task": s.id, "priority": s.priority, "sms": len(sms),
+                          "jobs": int(r.jobs), "wcrt_us": round(r.max_response_us, 1),
+                          "bound_us": float(bound), "ratio": round(ratio, 4),
+                          "mean_us": round(r.mean_response_us, 1),
+                          "max_kernel_us": round(r.max_kernel_us, 1),
+                          "gr_up_us": float(max(grs)), "deadline_us": d.deadline_us,
+                          "deadline_misses": int(r.deadline_misses)})
+    out.max_ratio = max(ratios)
+    out.all_within_bound = all(x <= 1.0 for x in ratios)
+    out.kernels_within_bound = kok
+    return out

@@ -1,0 +1,34 @@
+"""SM-partitioned persistent-thread executor on the B200: partition
+isolation (every participating block ran on an SM of its partition, two per
+SM), Eq. (1)-style scaling with SM count, and measured WCRT <= the RTGPU
+bound for concurrent tasks on disjoint partitions (BASELINE config 4)."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_partition_isolation_and_slots():
+    from paper_2101_10463_b200 import executor as ex
+    sms = [3, 4, 5, 6, 40, 41, 100, 147]
+    t, blocks, distinct = ex.kernel_ms(sms, 2, 2000, 256, reps=3)
+    assert blocks == 2 * len(sms), blocks      # -1 would mean a block ran outside
+    assert distinct == len(sms)
+    t1, b1, d1 = ex.kernel_ms([7], 1, 200, 256, reps=3)
+    assert b1 == 1 and d1 == 1
+
+
+def test_kernel_time_scales_with_partition():
+    from paper_2101_10463_b200 import executor as ex
+    one = min(ex.kernel_ms([0], 2, 800, 1024, reps=3)[0])
+    eight = min(ex.kernel_ms(list(range(8)), 2, 800, 1024, reps=3)[0])
+    assert 5.0 < one / eight < 9.0, (one, eight)
+
+
+def test_measured_wcrt_within_bound():
+    from paper_2101_10463_b200 import executor as ex
+    rep = ex.wcrt_experiment(n_tasks=4, m=3, horizon_us=1.5e6, seed=1)
+    assert rep.schedulable, rep.note
+    assert rep.kernels_within_bound, rep.tasks
+    assert rep.all_within_bound, rep.tasks
+    assert all(t["jobs"] > 0 for t in rep.tasks)
+    assert sum(rep.allocation.values()) // 2 <= 148
