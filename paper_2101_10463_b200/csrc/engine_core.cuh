@@ -458,6 +458,7 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
         /* stops inside the first (partial) job: the last x in [h, p-1] with
          * P[x] <= lim (P is non-decreasing; P[h] = base <= lim) */
         int x = h;
+#pragma unroll 5
         for (int st = half; st > 0; st >>= 1) {
             int y = x + st;
             if (y <= p - 1 && P[y] <= lim) x = y;
@@ -480,6 +481,7 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
             err = true;
             return 0;
         }
+#pragma unroll 5
         for (int st = half; st > 0; st >>= 1) {
             int y = x + st;
             if (y <= p - 2 && P[y] <= H2) x = y;
@@ -495,6 +497,7 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
         V k = Num<V>::floordiv(H2, C);
         Hs = H2 - k * C;
         w += k * EP[p];
+#pragma unroll 5
         for (int st = half; st > 0; st >>= 1) {
             int y = x + st;
             if (y <= p - 1 && P[y] <= Hs) x = y;
@@ -600,11 +603,17 @@ template <class V, class TM>
 RT_NI void lfp_many(const TM &tm, SetCtx<V> &c, int k, int kind, const V *bases, V *out, int cnt,
                     V bound, bool stop_on_none, bool &any_none) {
     any_none = false;
-    for (int j = 0; j < cnt; j++) {
+    unsigned done = 0;
+    for (int step = 0; step < cnt; step++) {
+        /* ascending base order, so every warm start has a predecessor */
+        int j = -1;
+        for (int q = 0; q < cnt; q++)
+            if (!((done >> q) & 1u) && (j < 0 || bases[q] < bases[j])) j = q;
+        done |= 1u << j;
         V b = bases[j], start = b;
         bool none = false;
-        for (int q = 0; q < j; q++) {
-            if (bases[q] <= b) {
+        for (int q = 0; q < cnt; q++) {
+            if (q != j && ((done >> q) & 1u) && bases[q] <= b) {
                 if (out[q] < 0) none = true;
                 else start = tmax(start, out[q] + (b - bases[q]));
             }
@@ -616,8 +625,8 @@ RT_NI void lfp_many(const TM &tm, SetCtx<V> &c, int k, int kind, const V *bases,
         if (r < 0) {
             any_none = true;
             if (stop_on_none) {
-                for (int q = j + 1; q < cnt; q++)
-                    if (tm.leader()) out[q] = (V)-1;
+                for (int q = 0; q < cnt; q++)
+                    if (!((done >> q) & 1u) && tm.leader()) out[q] = (V)-1;
                 tm.sync();
                 return;
             }
