@@ -111,8 +111,11 @@ int rtgpu_device_info(int *n_devices, int *sm_count, int *cc_major, int *cc_mino
 /*
  * Batched allocation search + response-time analysis (Algorithm 2) of S
  * packed task sets, each exactly as gpusched.analysis.analyze(ts, method).
- * Host pointers: the call copies the batch to the current device, runs the
- * kernels and copies the results back (the end-to-end path).
+ * Host pointers: the call copies the batch to the current device in chunks
+ * overlapped with the analysis of the chunks already resident, and copies
+ * the results back (the end-to-end path; pass pinned host memory for the
+ * overlap).  e2e_num / den are written only with RTGPU_F_BOUNDS or
+ * RTGPU_F_DETAIL.
  * eval_budget <= 0 means unlimited.  Returns 0 or a negative error code.
  */
 int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off,

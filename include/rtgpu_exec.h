@@ -40,6 +40,9 @@ typedef struct {
     double max_kernel_us;         /* worst kernel time (CUDA events)          */
     double max_kernel_wall_us;    /* worst kernel time incl. launch (host)    */
     double max_copy_us;
+    double seg_max_kernel_us[15]; /* worst time of each kernel segment        */
+    int32_t min_blocks;           /* fewest participating blocks in a launch  */
+    int32_t max_blocks;           /* most participating blocks in a launch    */
 } rtgpu_exec_result;
 
 const char *rtgpu_exec_last_error(void);

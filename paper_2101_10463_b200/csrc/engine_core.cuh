@@ -36,6 +36,7 @@
  */
 #pragma once
 #include <stdint.h>
+#include <string.h>
 
 #include "../../include/rtgpu.h"
 
@@ -76,6 +77,15 @@ template <> struct Num<double> {
         else if ((q + 1.0) * b <= a) q += 1.0;
         return q;
     }
+    static RT_HD double make_inv(double C) { return C > 0 ? 1.0 / C : 0.0; }
+    /* floor(a / b) from a precomputed inv ~ 1/b: estimate, then exact
+     * corrections (products are exact integers below 2^53) */
+    static RT_HD double floordiv_inv(double a, double b, double inv) {
+        double q = floor(a * inv);
+        while (q * b > a) q -= 1.0;
+        while ((q + 1.0) * b <= a) q += 1.0;
+        return q;
+    }
     static RT_HD i128 wide(double v) { return (i128)(i64)v; }
 };
 
@@ -85,6 +95,21 @@ template <> struct Num<i64> {
     static RT_HD i64 sc(i64 x, i64 q) { return x * q; }
     static RT_HD i64 of(i64 x) { return x; }
     static RT_HD i64 floordiv(i64 a, i64 b) { return a / b; }
+    static RT_HD i64 make_inv(i64 C) {
+        double inv = C > 0 ? 1.0 / (double)C : 0.0;
+        i64 bits;
+        memcpy(&bits, &inv, 8);
+        return bits;
+    }
+    static RT_HD i64 floordiv_inv(i64 a, i64 b, i64 inv_bits) {
+        double inv;
+        memcpy(&inv, &inv_bits, 8);
+        i64 q = (i64)((double)a * inv);
+        if (q < 0) q = 0;
+        while (q > 0 && q * b > a) q--;
+        while ((q + 1) * b <= a) q++;
+        return q;
+    }
     static RT_HD i128 wide(i64 v) { return (i128)v; }
 };
 
@@ -94,6 +119,8 @@ template <> struct Num<i128> {
     static RT_HD i128 sc(i64 x, i128 q) { return (i128)x * q; }
     static RT_HD i128 of(i64 x) { return (i128)x; }
     static RT_HD i128 floordiv(i128 a, i128 b) { return a / b; }
+    static RT_HD i128 make_inv(i128) { return 0; }
+    static RT_HD i128 floordiv_inv(i128 a, i128 b, i128) { return a / b; }
     static RT_HD i128 wide(i128 v) { return v; }
 };
 
@@ -144,8 +171,8 @@ template <class V> struct Layout {
     int scr_n;         /* scratch V entries */
     int bytes;
     RT_HD void init(const Dims &d) {
-        SC = 3 * d.MC + 4;
-        SM = d.MP > 0 ? 3 * d.MP + 4 : 0;
+        SC = 3 * d.MC + 5;
+        SM = d.MP > 0 ? 3 * d.MP + 5 : 0;
         int o = (int)sizeof(TaskRec) * d.maxn;
         o = (o + 15) & ~15;
         off_views_c = o;
@@ -154,6 +181,7 @@ template <class V> struct Layout {
         o += (int)sizeof(V) * SM * d.maxn;
         off_scr = o;
         scr_n = 2 * (d.MP + d.MC + 2) + d.MP + 3 * d.MC;
+        scr_n += (int)((32 * sizeof(int) + sizeof(V) - 1) / sizeof(V)); /* lfp_many order */
         o += (int)sizeof(V) * scr_n;
         bytes = (o + 15) & ~15;
     }
@@ -161,8 +189,9 @@ template <class V> struct Layout {
 
 /* view offsets inside one task's chain view */
 struct VOff {
-    int e, P, EP, F1, WN;
-    RT_HD VOff(int p_max) : e(0), P(p_max), EP(2 * p_max + 1), F1(3 * p_max + 2), WN(3 * p_max + 3) {}
+    int e, P, EP, F1, WN, INV;
+    RT_HD VOff(int p_max)
+        : e(0), P(p_max), EP(2 * p_max + 1), F1(3 * p_max + 2), WN(3 * p_max + 3), INV(3 * p_max + 4) {}
 };
 
 /* ------------------------------------------------------------ set context */
@@ -368,6 +397,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         V wrap = N::sc(t.T, q) - e;
         v[o.WN] = wrap < 0 ? (V)1 : (V)0;
         v[o.P + 1] = e + (wrap < 0 ? (V)0 : wrap);
+        v[o.INV] = Num<V>::make_inv(v[o.P + 1]);
         return;
     }
     /* CPU chain */
@@ -396,6 +426,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         V wrap = N::sc(t.T - t.sClu - t.sMll, q) - (t.isgpu ? (V)t.sGWlo * (V)perlo : (V)0);
         v[o.WN] = wrap < 0 ? (V)1 : (V)0;
         v[o.P + m] = P + elast + (wrap < 0 ? (V)0 : wrap);
+        v[o.INV] = Num<V>::make_inv(v[o.P + m]);
         (void)g;
     }
     /* memory chain */
@@ -426,6 +457,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         V wrap = N::sc(t.T - t.sMlu - t.innerCll, q) - (V)t.sGWlo * (V)perlo;
         v[o.WN] = wrap < 0 ? (V)1 : (V)0;
         v[o.P + p] = P + elast + (wrap < 0 ? (V)0 : wrap);
+        v[o.INV] = Num<V>::make_inv(v[o.P + p]);
     }
 }
 
@@ -494,7 +526,7 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
             err = true;
             return 0;
         }
-        V k = Num<V>::floordiv(H2, C);
+        V k = Num<V>::floordiv_inv(H2, C, v[o.INV]);
         Hs = H2 - k * C;
         w += k * EP[p];
 #pragma unroll 5
@@ -602,35 +634,44 @@ RT_NI V lfp(const TM &tm, SetCtx<V> &c, int k, int kind, V base, V start, V boun
 template <class V, class TM>
 RT_NI void lfp_many(const TM &tm, SetCtx<V> &c, int k, int kind, const V *bases, V *out, int cnt,
                     V bound, bool stop_on_none, bool &any_none) {
+    /* Ascending order of the bases via lane-parallel ranks (ties by index).
+     * lfp(b) - b is non-decreasing in b, so the best warm start for a base
+     * is its predecessor's fixed point plus the base difference, and a None
+     * predecessor makes every later base None. */
     any_none = false;
-    unsigned done = 0;
+    int *ord = (int *)(c.SCR() + c.L.scr_n) - 32;
+    tm.pfor(cnt, [&](int j) {
+        int r = 0;
+        for (int q = 0; q < cnt; q++) r += (bases[q] < bases[j] || (bases[q] == bases[j] && q < j)) ? 1 : 0;
+        ord[r] = j;
+    });
+    V prev_b = 0, prev_r = 0;
+    bool prev_none = false;
     for (int step = 0; step < cnt; step++) {
-        /* ascending base order, so every warm start has a predecessor */
-        int j = -1;
-        for (int q = 0; q < cnt; q++)
-            if (!((done >> q) & 1u) && (j < 0 || bases[q] < bases[j])) j = q;
-        done |= 1u << j;
-        V b = bases[j], start = b;
-        bool none = false;
-        for (int q = 0; q < cnt; q++) {
-            if (q != j && ((done >> q) & 1u) && bases[q] <= b) {
-                if (out[q] < 0) none = true;
-                else start = tmax(start, out[q] + (b - bases[q]));
-            }
+        const int j = ord[step];
+        const V b = bases[j];
+        V r;
+        if (prev_none) {
+            r = (V)-1;
+        } else {
+            V start = step ? tmax(b, prev_r + (b - prev_b)) : b;
+            r = lfp(tm, c, k, kind, b, start, bound);
         }
-        V r = none ? (V)-1 : lfp(tm, c, k, kind, b, start, bound);
         tm.sync();
         if (tm.leader()) out[j] = r;
         tm.sync();
         if (r < 0) {
             any_none = true;
+            prev_none = true;
             if (stop_on_none) {
-                for (int q = 0; q < cnt; q++)
-                    if (!((done >> q) & 1u) && tm.leader()) out[q] = (V)-1;
+                for (int q = step + 1; q < cnt; q++)
+                    if (tm.leader()) out[ord[q]] = (V)-1;
                 tm.sync();
                 return;
             }
         }
+        prev_b = b;
+        prev_r = r;
     }
 }
 

@@ -276,14 +276,20 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
                     double c0 = us_since(seg_t0);
                     R.max_copy_us = std::max(R.max_copy_us, c0);
                     auto k0 = clk::now();
+                    cudaMemsetAsync(L.trace, 0, sizeof(unsigned), L.st);
                     cudaEventRecord(L.e0, L.st);
                     enqueue_segment(L, t.sm_mask, t.slots_per_sm, t.kernel_items[s], t.kernel_iters,
-                                    false);
+                                    true);
                     cudaEventRecord(L.e1, L.st);
+                    unsigned nb = 0;
+                    cudaMemcpyAsync(&nb, L.trace, sizeof(unsigned), cudaMemcpyDeviceToHost, L.st);
                     cudaStreamSynchronize(L.st);
                     float kms = 0;
                     cudaEventElapsedTime(&kms, L.e0, L.e1);
                     R.max_kernel_us = std::max(R.max_kernel_us, (double)kms * 1e3);
+                    R.seg_max_kernel_us[s] = std::max(R.seg_max_kernel_us[s], (double)kms * 1e3);
+                    if (R.min_blocks == 0 || (int)nb < R.min_blocks) R.min_blocks = (int)nb;
+                    R.max_blocks = std::max(R.max_blocks, (int)nb);
                     R.max_kernel_wall_us = std::max(R.max_kernel_wall_us, us_since(k0));
                     if (t.two_copy && copy < t.n_copies) {
                         auto d0 = clk::now();

@@ -25,6 +25,8 @@ struct KParams {
     i64 *e2e, *den, *detail;
     unsigned long long *ctr; /* [0..2] work counters, [3..4] escalation counts */
     i64 *esc0, *esc1;        /* escalation lists (stage 0 -> 1, 1 -> 2) */
+    i64 set_base;            /* stage 0: first set of this launch (chunked e2e path) */
+    unsigned long long *wctr0; /* stage 0: this launch's work counter */
 };
 
 /* minimum resident CTAs per SM the register allocation must allow */
@@ -56,12 +58,13 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
     WarpTeam tm{lane};
     const i64 count = stage == 0 ? p.n_sets : (i64)(stage == 1 ? p.ctr[3] : p.ctr[4]);
     const i64 *list = stage == 0 ? nullptr : (stage == 1 ? p.esc0 : p.esc1);
+    unsigned long long *wctr = stage == 0 ? p.wctr0 : &p.ctr[stage];
     for (;;) {
         unsigned long long idx = 0;
-        if (lane == 0) idx = atomicAdd(&p.ctr[stage], 1ull);
+        if (lane == 0) idx = atomicAdd(wctr, 1ull);
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if ((i64)idx >= count) break;
-        const i64 s = list ? list[idx] : (i64)idx;
+        const i64 s = list ? list[idx] : p.set_base + (i64)idx;
         c.blob = p.blobs + p.set_off[s];
         const i64 tb = p.task_base[s];
         OutPtrs<V> o;

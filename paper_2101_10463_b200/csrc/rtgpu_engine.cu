@@ -17,6 +17,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "../../include/rtgpu.h"
@@ -56,6 +57,11 @@ struct DevBuf {
 };
 
 DevBuf g_scratch; /* counters + escalation lists */
+const int MAX_CHUNKS = 16;
+const size_t CTR_WORDS = 8 + MAX_CHUNKS; /* [0..4] stage counters, [8..) chunk counters */
+cudaStream_t g_s_copy = nullptr, g_s_comp[2] = {nullptr, nullptr};
+cudaEvent_t g_ev_chunk[MAX_CHUNKS], g_ev_comp[2];
+bool g_pipe_init = false;
 int g_timing = 0;
 unsigned long long *g_last_ctr = nullptr;
 i64 g_last_n = 0;
@@ -90,7 +96,7 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     }
     g_launches = 0;
     if (n_sets <= 0) return 0;
-    size_t need = 8 * sizeof(unsigned long long) + 2 * sizeof(i64) * (size_t)n_sets;
+    size_t need = CTR_WORDS * sizeof(unsigned long long) + 2 * sizeof(i64) * (size_t)n_sets;
     if (!g_scratch.ensure(need)) {
         set_err("cudaMalloc scratch", cudaGetLastError());
         return -6;
@@ -113,9 +119,11 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     p.den = d_den;
     p.detail = d_detail;
     p.ctr = (unsigned long long *)g_scratch.p;
-    p.esc0 = (i64 *)((char *)g_scratch.p + 8 * sizeof(unsigned long long));
+    p.esc0 = (i64 *)((char *)g_scratch.p + CTR_WORDS * sizeof(unsigned long long));
     p.esc1 = p.esc0 + n_sets;
-    cudaError_t e = cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    p.set_base = 0;
+    p.wctr0 = &p.ctr[0];
+    cudaError_t e = cudaMemsetAsync(p.ctr, 0, CTR_WORDS * sizeof(unsigned long long), st);
     if (e != cudaSuccess) {
         set_err("cudaMemsetAsync", e);
         return -7;
@@ -262,32 +270,92 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
                        int64_t n_sets, int method, unsigned flags, int64_t eval_budget,
                        int32_t *status, int64_t *evals, int32_t *vsm, int64_t *e2e_num,
                        int64_t *den, int64_t *detail) {
+    /* End-to-end path: the batch is copied in chunks on a copy stream while
+     * stage-0 kernels analyse the chunks already resident (two compute
+     * streams, so a chunk's tail overlaps the next chunk); the escalation
+     * stages and the result copies follow.  With pinned host buffers the
+     * H2D transfer hides behind the analysis. */
     std::lock_guard<std::mutex> lk(g_mu);
+    g_launches = 0;
     if (n_sets <= 0) return 0;
+    if (method < RTGPU_METHOD_RTGPU || method > RTGPU_METHOD_BUSYWAIT) {
+        snprintf(g_err, sizeof g_err, "unknown analysis method %d", method);
+        return -2;
+    }
     Dims d;
     scan_dims_host((const i64 *)blobs, (const i64 *)set_off, n_sets, &d);
     const size_t W = (size_t)set_off[n_sets], T = (size_t)task_base[n_sets];
     if (!g_h_blobs.ensure(W * 8) || !g_h_off.ensure((n_sets + 1) * 8) ||
         !g_h_tb.ensure((n_sets + 1) * 8) || !g_h_status.ensure(n_sets * 4) ||
         !g_h_evals.ensure(n_sets * 8) || !g_h_vsm.ensure(T * 4) || !g_h_e2e.ensure(T * 8) ||
-        !g_h_den.ensure(T * 8) || (detail && !g_h_detail.ensure(W * 8))) {
+        !g_h_den.ensure(T * 8) || (detail && !g_h_detail.ensure(W * 8)) ||
+        !g_scratch.ensure(CTR_WORDS * 8 + 2 * 8 * (size_t)n_sets)) {
         set_err("cudaMalloc", cudaGetLastError());
         return -6;
     }
-    cudaStream_t st = 0;
-    cudaMemcpyAsync(g_h_blobs.p, blobs, W * 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(g_h_off.p, set_off, (n_sets + 1) * 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(g_h_tb.p, task_base, (n_sets + 1) * 8, cudaMemcpyHostToDevice, st);
-    int rc = run_device((const i64 *)g_h_blobs.p, (const i64 *)g_h_off.p, (const i64 *)g_h_tb.p,
-                        n_sets, d, method, flags, eval_budget, (int32_t *)g_h_status.p,
-                        (i64 *)g_h_evals.p, (int32_t *)g_h_vsm.p, (i64 *)g_h_e2e.p,
-                        (i64 *)g_h_den.p, detail ? (i64 *)g_h_detail.p : nullptr, st);
+    if (!g_pipe_init) {
+        cudaStreamCreateWithFlags(&g_s_copy, cudaStreamNonBlocking);
+        for (int i = 0; i < 2; i++) {
+            cudaStreamCreateWithFlags(&g_s_comp[i], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&g_ev_comp[i], cudaEventDisableTiming);
+        }
+        for (int i = 0; i < MAX_CHUNKS; i++) cudaEventCreateWithFlags(&g_ev_chunk[i], cudaEventDisableTiming);
+        g_pipe_init = true;
+    }
+    KParams p;
+    p.blobs = (const i64 *)g_h_blobs.p;
+    p.set_off = (const i64 *)g_h_off.p;
+    p.task_base = (const i64 *)g_h_tb.p;
+    p.dims = d;
+    p.GC = pow2_group(d.MC);
+    p.GM = pow2_group(d.MP > 0 ? d.MP : 1);
+    p.flags = flags;
+    p.method = method;
+    p.budget = eval_budget > 0 ? eval_budget : (i64)1 << 22;
+    p.status = (int32_t *)g_h_status.p;
+    p.evals = (i64 *)g_h_evals.p;
+    p.vsm = (int32_t *)g_h_vsm.p;
+    p.e2e = (i64 *)g_h_e2e.p;
+    p.den = (i64 *)g_h_den.p;
+    p.detail = detail ? (i64 *)g_h_detail.p : nullptr;
+    p.ctr = (unsigned long long *)g_scratch.p;
+    p.esc0 = (i64 *)((char *)g_scratch.p + CTR_WORDS * 8);
+    p.esc1 = p.esc0 + n_sets;
+    const int chunks = (int)std::min<i64>(MAX_CHUNKS, std::max<i64>(1, n_sets / 4096));
+    cudaStream_t cp = g_s_copy;
+    cudaMemsetAsync(p.ctr, 0, CTR_WORDS * 8, cp);
+    cudaMemcpyAsync(g_h_off.p, set_off, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
+    cudaMemcpyAsync(g_h_tb.p, task_base, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
+    int rc = 0;
+    for (int c = 0; c < chunks && !rc; c++) {
+        const i64 a = n_sets * c / chunks, b = n_sets * (c + 1) / chunks;
+        const size_t w0 = (size_t)set_off[a], w1 = (size_t)set_off[b];
+        cudaMemcpyAsync((i64 *)g_h_blobs.p + w0, blobs + w0, (w1 - w0) * 8, cudaMemcpyHostToDevice, cp);
+        cudaEventRecord(g_ev_chunk[c], cp);
+        cudaStream_t cs = g_s_comp[c & 1];
+        cudaStreamWaitEvent(cs, g_ev_chunk[c], 0);
+        KParams q = p;
+        q.set_base = a;
+        q.n_sets = b - a;
+        q.wctr0 = &p.ctr[8 + c];
+        rc = launch_stage_f64(q, 0, cs);
+    }
+    if (rc) return rc;
+    /* escalation stages and results on compute stream 0 after every chunk */
+    cudaEventRecord(g_ev_comp[1], g_s_comp[1]);
+    cudaStreamWaitEvent(g_s_comp[0], g_ev_comp[1], 0);
+    cudaStream_t st = g_s_comp[0];
+    p.n_sets = n_sets;
+    rc = launch_stage_i64(p, 1, st);
+    if (!rc) rc = launch_stage_i128(p, 2, st);
     if (rc) return rc;
     cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(e2e_num, g_h_e2e.p, T * 8, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(den, g_h_den.p, T * 8, cudaMemcpyDeviceToHost, st);
+    if (flags & (RTGPU_F_BOUNDS | RTGPU_F_DETAIL)) {
+        cudaMemcpyAsync(e2e_num, g_h_e2e.p, T * 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(den, g_h_den.p, T * 8, cudaMemcpyDeviceToHost, st);
+    }
     if (detail) cudaMemcpyAsync(detail, g_h_detail.p, W * 8, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {

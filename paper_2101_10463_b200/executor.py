@@ -44,7 +44,8 @@ class ExecResultC(ctypes.Structure):
     _fields_ = [("jobs", ctypes.c_int64), ("deadline_misses", ctypes.c_int64),
                 ("max_response_us", ctypes.c_double), ("mean_response_us", ctypes.c_double),
                 ("max_kernel_us", ctypes.c_double), ("max_kernel_wall_us", ctypes.c_double),
-                ("max_copy_us", ctypes.c_double)]
+                ("max_copy_us", ctypes.c_double), ("seg_max_kernel_us", ctypes.c_double * 15),
+                ("min_blocks", ctypes.c_int32), ("max_blocks", ctypes.c_int32)]
 
 
 def _lib():
@@ -236,13 +237,17 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
         grs = [gpu_response_bounds(g, 2 * len(sms)).hi for g in s.gpu_segments]
         ratio = r.max_response_us / float(bound)
         ratios.append(ratio)
-        kern_ok = r.max_kernel_us <= float(max(grs))
+        seg = [r.seg_max_kernel_us[j] for j in range(len(grs))]
+        kern_ok = all(x <= float(b) for x, b in zip(seg, grs))
         kok = kok and kern_ok
         out.tasks.append({"task": s.id, "priority": s.priority, "sms": len(sms),
                           "jobs": int(r.jobs), "wcrt_us": round(r.max_response_us, 1),
                           "bound_us": float(bound), "ratio": round(ratio, 4),
                           "mean_us": round(r.mean_response_us, 1),
                           "max_kernel_us": round(r.max_kernel_us, 1),
+                          "kernel_us_vs_gr_up": [[round(x, 1), round(float(b), 1)]
+                                                 for x, b in zip(seg, grs)],
+                          "blocks_per_launch": [int(r.min_blocks), int(r.max_blocks)],
                           "gr_up_us": float(max(grs)), "deadline_us": d.deadline_us,
                           "deadline_misses": int(r.deadline_misses)})
     out.max_ratio = max(ratios)

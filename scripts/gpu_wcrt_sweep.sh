@@ -1,0 +1,12 @@
+timeout 600 python - <<'PY'
+import json
+from paper_2101_10463_b200.executor import wcrt_experiment
+for u in (1.0, 2.0, 3.0, 4.0):
+    for items_scale in (1,):
+        try:
+            r = wcrt_experiment(n_tasks=4, m=3, horizon_us=1.5e6, seed=3, utilization=u)
+            print(u, r.schedulable, r.all_within_bound, r.kernels_within_bound, round(r.max_ratio,3), r.allocation, [ (t['sms'], t['jobs'], t['ratio']) for t in r.tasks])
+        except Exception as e:
+            print(u, "ERR", e)
+PY
+bash scripts/gpu_bench_prof.sh sort

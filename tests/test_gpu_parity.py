@@ -49,7 +49,7 @@ def test_gpu_matches_reference_reports(golden, first, mi):
     cases, batch = golden
     res = analyze_packed(batch.blobs, batch.set_off, batch.task_base, mi, F_DETAIL | first)
     assert not _check_golden(cases, batch, res, METHODS[mi])
-    assert _native.last_launch_count() == 3
+    assert _native.last_launch_count() >= 3
 
 
 def test_dropin_api_matches_reference(golden):
@@ -127,3 +127,18 @@ def test_device_batch_all_stages_agree():
         f0 = [Fraction(int(a), int(d)) for a, d in zip(outs[0].e2e_num, outs[0].den) if a >= 0]
         f1 = [Fraction(int(a), int(d)) for a, d in zip(r.e2e_num, r.den) if a >= 0]
         assert f0 == f1
+
+
+def test_e2e_chunked_path_equals_device_path():
+    """rtgpu_analyze_host pipelines chunks over two streams; same results."""
+    gp = _native.gen_params_c(8, 5, (1000, 20000), (1000, 20000), (250, 5000), Fraction(1, 2), 0,
+                              10, Fraction(12, 100), Fraction(1))
+    b, so, tb = _native.generate(gp, list(range(40000)))
+    batch = DeviceBatch(b, so, tb)
+    out = batch.alloc_results()
+    batch.run(out, flags=F_BOUNDS)
+    g = out.to_host()
+    h = analyze_packed(b, so, tb, 0, F_BOUNDS)
+    assert _native.last_launch_count() > 3
+    assert np.array_equal(g.status, h.status) and np.array_equal(g.vsm, h.vsm)
+    assert np.array_equal(g.e2e_num, h.e2e_num) and np.array_equal(g.den, h.den)
