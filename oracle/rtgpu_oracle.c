@@ -685,6 +685,46 @@ static void write_report(const oset *s, const aview *av, const trep *rep, int me
     }
 }
 
+/* Greedy restatement (flags & ORACLE_GREEDY): each GPU task in priority
+ * order takes the smallest count at which the faithful per-allocation
+ * evaluation (eval_rtgpu: literal walks and literal iteration) passes it,
+ * given the counts already chosen; later tasks sit at their minimum (they do
+ * not influence earlier tasks).  DESIGN.md section 3 shows this equals the
+ * reference's lexicographic grid search for regular task sets; tests check
+ * it against the full enumeration above on small sets and use it as the
+ * checker where the enumeration cannot finish (148 SMs). */
+static int greedy_rtgpu(octx *c, const oset *s, const int *mins, int *gn, aview *av, trep *rep) {
+    for (int k = 0; k < s->n; k++) gn[k] = s->t[k].g > 0 ? mins[k] : 0;
+    int64_t used = 0;
+    for (int k = 0; k < s->n; k++) {
+        const otask *t = &s->t[k];
+        if (t->g == 0) {
+            build_view(c, s, gn, av);
+            eval_rtgpu(c, av, rep);
+            if (!rep[k].present || rep[k].e2e == NONE128) return 0;
+            continue;
+        }
+        int64_t after = 0;
+        for (int i = k + 1; i < s->n; i++)
+            if (s->t[i].g > 0) after += mins[i];
+        int64_t gmax = s->gn - used - after;
+        int found = 0;
+        for (int g = mins[k]; g <= gmax && !found; g++) {
+            gn[k] = g;
+            build_view(c, s, gn, av);
+            eval_rtgpu(c, av, rep);
+            /* task k passes iff the evaluation got past it */
+            if (rep[k].present && rep[k].e2e != NONE128 && rep[k].e2e <= av->v[k].D) found = g;
+        }
+        if (!found) return 0;
+        gn[k] = found;
+        used += found;
+    }
+    return 1;
+}
+
+#define ORACLE_GREEDY 0x100u
+
 int oracle_analyze_set(const int64_t *blob, int method, unsigned flags, int64_t budget,
                        int32_t *status, int64_t *evals, int32_t *vsm, int64_t *e2e_num,
                        int64_t *den, int64_t *blob_detail) {
@@ -736,6 +776,30 @@ int oracle_analyze_set(const int64_t *blob, int method, unsigned flags, int64_t 
             if (iso > t->D) goto unsched_empty;
             mins[k] = 0;
         }
+    }
+    if ((flags & ORACLE_GREEDY) && method == RTGPU_METHOD_RTGPU) {
+        int64_t need = 0;
+        for (int q = 0; q < nid; q++) need += mins[ids[q]];
+        if (need > s.gn) goto unsched_empty;
+        int ok = greedy_rtgpu(&c, &s, mins, gn, &av, rep);
+        *status = ok ? RTGPU_SCHEDULABLE : RTGPU_UNSCHEDULABLE;
+        *evals = c.evals;
+        if (!ok) {
+            /* the reference reports the lexicographically last allocation */
+            int first = -1;
+            int64_t others = 0;
+            for (int q = 0; q < nid; q++) {
+                if (first < 0) first = ids[q];
+                else others += mins[ids[q]];
+            }
+            for (int k = 0; k < s.n; k++)
+                gn[k] = s.t[k].g > 0 ? (k == first ? (int)(s.gn - others) : mins[k]) : 0;
+        }
+        build_view(&c, &s, gn, &av);
+        eval_rtgpu(&c, &av, rep);
+        write_report(&s, &av, rep, method, gn, ok, blob_detail, vsm, e2e_num, den, &range_err);
+        if (range_err) *status = RTGPU_RANGE;
+        return 0;
     }
     {
         /* gpu.py:43 _compositions in lexicographic order */
