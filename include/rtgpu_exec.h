@@ -53,6 +53,11 @@ const char *rtgpu_exec_last_error(void);
 int rtgpu_exec_kernel_ms(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
                          float *ms_out, int32_t *blocks_out, int32_t *sms_out);
 
+/* Same, with the GPU left idle for idle_us before every timed launch (the
+ * clock may have dropped: worst-case calibration without locked clocks). */
+int rtgpu_exec_kernel_ms_idle(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
+                              int idle_us, float *ms_out, int32_t *blocks_out, int32_t *sms_out);
+
 /* Time `reps` pinned-host copies of `bytes` (to_device: H2D, else D2H). */
 int rtgpu_exec_copy_ms(int64_t bytes, int to_device, int reps, float *ms_out);
 

@@ -86,6 +86,24 @@ template <> struct Num<double> {
         while ((q + 1.0) * b <= a) q += 1.0;
         return q;
     }
+    /* q = floor(a / b) and r = a - q b (a >= 0, b > 0, integers < 2^52):
+     * the fma remainder is exact, one correction covers the estimate's error */
+    static RT_HD double divmod_inv(double a, double b, double inv, double &r) {
+        double q = floor(a * inv);
+        r = fma(-q, b, a);
+        if (r < 0) {
+            q -= 1.0;
+            r += b;
+        } else if (r >= b) {
+            q += 1.0;
+            r -= b;
+        }
+        if (r < 0 || r >= b) { /* never for |a| < 2^52; kept for safety */
+            q = floordiv(a, b);
+            r = a - q * b;
+        }
+        return q;
+    }
     static RT_HD i128 wide(double v) { return (i128)(i64)v; }
 };
 
@@ -100,6 +118,11 @@ template <> struct Num<i64> {
         i64 bits;
         memcpy(&bits, &inv, 8);
         return bits;
+    }
+    static RT_HD i64 divmod_inv(i64 a, i64 b, i64 inv_bits, i64 &r) {
+        i64 q = floordiv_inv(a, b, inv_bits);
+        r = a - q * b;
+        return q;
     }
     static RT_HD i64 floordiv_inv(i64 a, i64 b, i64 inv_bits) {
         double inv;
@@ -121,6 +144,11 @@ template <> struct Num<i128> {
     static RT_HD i128 floordiv(i128 a, i128 b) { return a / b; }
     static RT_HD i128 make_inv(i128) { return 0; }
     static RT_HD i128 floordiv_inv(i128 a, i128 b, i128) { return a / b; }
+    static RT_HD i128 divmod_inv(i128 a, i128 b, i128, i128 &r) {
+        i128 q = a / b;
+        r = a - q * b;
+        return q;
+    }
     static RT_HD i128 wide(i128 v) { return v; }
 };
 
@@ -130,6 +158,15 @@ template <class T> RT_HD T tmin(T a, T b) { return a < b ? a : b; }
 template <class T> RT_HD T gcdq(T a, T b) {
     if (a < 0) a = -a;
     if (b < 0) b = -b;
+    if (a <= (T)0x7fffffff && b <= (T)0x7fffffff) { /* native 32-bit remainder */
+        unsigned x = (unsigned)a, y = (unsigned)b;
+        while (y != 0) {
+            unsigned t = x % y;
+            x = y;
+            y = t;
+        }
+        return (T)x;
+    }
     while (b != 0) {
         T t = a % b;
         a = b;
@@ -226,6 +263,7 @@ template <class V> struct SetCtx {
     int stuck;          /* fixed point iteration cap hit */
     i64 evals, budget;
     int budget_hit;
+    Qt fixed_q; /* 2*A*lcm(1..GN) when it fits the stage: one scale for the whole search */
 };
 
 #ifdef __CUDACC__
@@ -526,8 +564,7 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
             err = true;
             return 0;
         }
-        V k = Num<V>::floordiv_inv(H2, C, v[o.INV]);
-        Hs = H2 - k * C;
+        V k = Num<V>::divmod_inv(H2, C, v[o.INV], Hs);
         w += k * EP[p];
 #pragma unroll 5
         for (int st = half; st > 0; st >>= 1) {
@@ -688,6 +725,7 @@ template <class V> struct TaskEval {
 template <class V>
 RT_HD typename Num<V>::Qt task_scale(SetCtx<V> &c, int k, int g, typename Num<V>::Qt lcm_pre) {
     typedef typename Num<V>::Qt Qt;
+    if (c.fixed_q) return c.fixed_q; /* multiple of every 2*A*g: views never rescale */
     Qt q = lcm_lim<Qt>(lcm_pre, (Qt)1, c.qlim);
     q = (q == 0 || q > c.qlim / 2) ? 0 : q * 2;
     if (q != 0 && c.TR()[k].isgpu) q = lcm_lim<Qt>(q, (Qt)2 * (Qt)c.A * (Qt)g, c.qlim);
@@ -1397,6 +1435,7 @@ RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 ho
     c.stuck = 0;
     c.evals = 0;
     c.single_seg = 0;
+    c.fixed_q = 0;
     if (c.n < 1 || c.n > c.maxn || c.A < 1 || k < 0 || k >= c.n) return RTGPU_INVALID;
     i128 vb_max = 0;
     tm.pfor(c.n, [&](int i) {
@@ -1537,6 +1576,12 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
     if (vb > (i128)Num<V>::limit()) return ST_ESCALATE;
     c.Vb = (i64)vb;
     c.qlim = (Qt)(Num<V>::limit() / (Qt)c.Vb);
+    c.fixed_q = 0;
+    if (c.method == RTGPU_METHOD_RTGPU && c.GN >= 1 && c.GN <= 64) {
+        Qt L = 1;
+        for (int g = 2; g <= c.GN && L != 0; g++) L = lcm_lim<Qt>(L, (Qt)g, c.qlim);
+        if (L != 0 && L <= c.qlim / (2 * (Qt)c.A)) c.fixed_q = L * 2 * (Qt)c.A;
+    }
     tm.sync();
     /* mem blocking term of analysis.py:162: longest copy of any lower-priority task */
     tm.pfor(c.n, [&](int k) {

@@ -60,20 +60,25 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
         unsigned pos = atomicAdd(&a.trace[0], 1u);
         if (pos < 4095) a.trace[1 + pos] = sm;
     }
-    /* synthetic compute work: dependent FMA chains, 4 per thread (ILP) */
+    /* synthetic compute work: dependent FMA chains, 4 per thread (ILP).
+     * The next item is claimed before the current one is computed, so the
+     * atomic's round trip (L2-die and contention dependent) overlaps work. */
     float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f, x3 = x0 + 3.f;
-    for (;;) {
-        if (threadIdx.x == 0) item = atomicAdd(a.work, 1ull);
-        __syncthreads();
-        const unsigned long long it = item;
-        __syncthreads();
-        if ((long long)it >= a.items) break;
+    __shared__ unsigned long long next;
+    if (threadIdx.x == 0) item = atomicAdd(a.work, 1ull);
+    __syncthreads();
+    unsigned long long it = item;
+    while ((long long)it < a.items) {
+        if (threadIdx.x == 0) next = atomicAdd(a.work, 1ull);
         for (int k = 0; k < a.iters; k++) {
             x0 = fmaf(x0, 0.9999999f, 0.5f);
             x1 = fmaf(x1, 0.9999999f, 0.5f);
             x2 = fmaf(x2, 0.9999999f, 0.5f);
             x3 = fmaf(x3, 0.9999999f, 0.5f);
         }
+        __syncthreads();
+        it = next;
+        __syncthreads();
     }
     if (x0 + x1 + x2 + x3 == 12345.f) a.sink[blockIdx.x] = x0;
 }
@@ -164,6 +169,11 @@ const char *rtgpu_exec_last_error(void) { return g_err; }
 
 int rtgpu_exec_kernel_ms(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
                          float *ms_out, int32_t *blocks_out, int32_t *sms_out) {
+    return rtgpu_exec_kernel_ms_idle(mask, nslots, items, iters, reps, 0, ms_out, blocks_out, sms_out);
+}
+
+int rtgpu_exec_kernel_ms_idle(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
+                              int idle_us, float *ms_out, int32_t *blocks_out, int32_t *sms_out) {
     Lane L;
     if (lane_init(L, 64)) {
         strcpy(g_err, "executor allocation failed");
@@ -173,6 +183,7 @@ int rtgpu_exec_kernel_ms(const uint32_t *mask, int nslots, int64_t items, int it
     enqueue_segment(L, mask, nslots, items, iters, false);
     cudaStreamSynchronize(L.st);
     for (int r = 0; r < reps; r++) {
+        if (idle_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(idle_us));
         cudaEventRecord(L.e0, L.st);
         enqueue_segment(L, mask, nslots, items, iters, r == 0);
         cudaEventRecord(L.e1, L.st);

@@ -56,6 +56,11 @@ def _lib():
                                            ctypes.POINTER(ctypes.c_float),
                                            ctypes.POINTER(ctypes.c_int32),
                                            ctypes.POINTER(ctypes.c_int32)]
+        L.rtgpu_exec_kernel_ms_idle.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_int,
+                                                ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_int, ctypes.POINTER(ctypes.c_float),
+                                                ctypes.POINTER(ctypes.c_int32),
+                                                ctypes.POINTER(ctypes.c_int32)]
         L.rtgpu_exec_copy_ms.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_float)]
         L.rtgpu_exec_run.argtypes = [ctypes.POINTER(ExecTaskC), ctypes.c_int, ctypes.c_double,
@@ -72,15 +77,15 @@ def mask_of(sms) -> "ctypes.Array":
     return m
 
 
-def kernel_ms(sms, nslots: int, items: int, iters: int, reps: int = 5):
-    """Times (ms) of `reps` launches on the SM list; also participating blocks
-    of the first launch (-1 if a block ran outside the partition) and the
-    number of distinct SMs that ran it."""
+def kernel_ms(sms, nslots: int, items: int, iters: int, reps: int = 5, idle_us: int = 0):
+    """Times (ms) of `reps` launches on the SM list (each after idle_us of an
+    idle GPU); also participating blocks of the first launch (-1 if a block
+    ran outside the partition) and the number of distinct SMs that ran it."""
     _native.require_device()
     out = (ctypes.c_float * reps)()
     nb, ns = ctypes.c_int32(0), ctypes.c_int32(0)
-    rc = _lib().rtgpu_exec_kernel_ms(mask_of(sms), nslots, items, iters, reps, out,
-                                     ctypes.byref(nb), ctypes.byref(ns))
+    rc = _lib().rtgpu_exec_kernel_ms_idle(mask_of(sms), nslots, items, iters, reps, idle_us, out,
+                                          ctypes.byref(nb), ctypes.byref(ns))
     if rc:
         raise RuntimeError(_lib().rtgpu_exec_last_error().decode())
     return [float(x) for x in out], nb.value, ns.value
@@ -129,10 +134,17 @@ def _ceil_margin(x_us: float, margin: float) -> int:
     return int(math.ceil(x_us * (1 + margin))) + 1
 
 
-def calibrate_kernel(items: int, iters: int, reps: int = 5, margin: float = 0.08,
-                     sm: int = 0) -> KernelCal:
-    t1 = kernel_ms([sm], 1, items, iters, reps)[0]
-    t2 = kernel_ms([sm], 2, items, iters, reps)[0]
+CAL_SMS = (0, 74)  # one SM on each die: L2 distance differs per die
+
+
+def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = 0.12,
+                     idle_us: int = 20000) -> KernelCal:
+    """Worst case over SMs of both dies, warm launches and launches after an
+    idle GPU (the SM clock may have dropped; clocks are not locked here)."""
+    t1, t2 = [], []
+    for sm in CAL_SMS:
+        t1 += kernel_ms([sm], 1, items, iters, reps)[0] + kernel_ms([sm], 1, items, iters, 2, idle_us)[0]
+        t2 += kernel_ms([sm], 2, items, iters, reps)[0] + kernel_ms([sm], 2, items, iters, 2, idle_us)[0]
     t1u, t2u = max(t1) * 1e3, max(t2) * 1e3
     alpha = Fraction(max(100, min(180, math.ceil(200 * t2u / t1u))), 100)
     return KernelCal(items, iters, t1u, t2u, alpha, int(min(t1) * 1e3 * 0.95),
@@ -169,8 +181,8 @@ def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = 
 
 
 def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int = 0,
-                    utilization: float = 0.45, horizon_us: float = 3e6, n_sm: int = 148,
-                    margin: float = 0.08) -> WcrtReport:
+                    utilization: float = 3.0, horizon_us: float = 3e6, n_sm: int = 148,
+                    margin: float = 0.12) -> WcrtReport:
     """BASELINE config 4: n concurrent tasks on disjoint SM partitions of the
     GPU; measured WCRT vs the RTGPU bound R_k."""
     _native.require_device()
@@ -187,7 +199,8 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
         for it in d.kernel_items:
             if it not in cal:
                 cal[it] = calibrate_kernel(it, iters, margin=margin)
-    overhead = max(kernel_ms(list(range(8)), 2, 0, iters, 5)[0]) * 1e3
+    overhead = max(kernel_ms(list(range(8)), 2, 0, iters, 5)[0] +
+                   kernel_ms(list(range(8)), 2, 0, iters, 3, 20000)[0]) * 1e3
     GL = _ceil_margin(overhead, margin)
     copy_cal = {}
     for d in defs:
