@@ -771,6 +771,30 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
     /* memory segments: analysis.py:156 (blocking = longest lp copy) */
     V sum_mr = 0;
     bool mr_none = false;
+    const V grup = sum_grup(c, k, g, q);
+    if (t.p > 0 && !want_all) {
+        /* Verdict shortcut, exact: lfp(b') >= lfp(b) + (b' - b) gives
+         * MR_j <= lfp(b_max) - (b_max - b_j), and lfp(b_max) is MR of the
+         * longest copy.  One fixed point decides "some MR is None"; if R2
+         * passes with the resulting upper bound on sum MR it passes exactly
+         * (the least fixed point is monotone in the base). */
+        i64 bmax_t = 0, bsum_t = 0;
+        for (int j = 0; j < t.p; j++) {
+            bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
+            bsum_t += ml_hi[j] + t.B;
+        }
+        const V bmax = N::sc(bmax_t, q);
+        const V rmax = lfp(tm, c, k, K_MEM, bmax, bmax, D);
+        if (rmax < 0) return; /* the longest copy's MR is None: task fails */
+        const V mr_ub = (V)t.p * (rmax - bmax) + N::sc(bsum_t, q);
+        const V b2 = grup + mr_ub + N::sc(t.sClu, q);
+        const V r2ub = lfp(tm, c, k, K_CPU, b2, b2, D);
+        if (r2ub >= 0) {
+            res.pass = true;
+            res.e2e = r2ub; /* an upper bound; verdict mode reports no bounds */
+            return;
+        }
+    }
     if (t.p > 0) {
         tm.pfor(t.p, [&](int j) { bases[j] = N::sc(ml_hi[j] + t.B, q); });
         lfp_many(tm, c, k, K_MEM, bases, outs, t.p, D, !want_all, mr_none);
@@ -780,7 +804,6 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
         tm.sync();
         if (mr_none && !want_all) return;
     }
-    const V grup = sum_grup(c, k, g, q);
     /* end_to_end R2 (analysis.py:214) first: it needs no per-segment CPU bounds */
     V r2 = (V)-1;
     if (!mr_none) r2 = lfp(tm, c, k, K_CPU, grup + sum_mr + N::sc(t.sClu, q),
@@ -1413,6 +1436,253 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
     }
 }
 
+/* ------------------------------------------------------------ verdict fast path */
+
+/* The hot case of the benchmark -- RTGPU verdicts (status + allocation) of
+ * regular task sets whose whole search fits one FP64 scale Q = 2*A*lcm(1..GN)
+ * -- as one compact routine: everything warp-uniform lives in registers or
+ * shared memory, the only out-of-line callee is the fixed point below, which
+ * takes scalars (no context on the stack), so the hot code stays inside the
+ * instruction cache.  Same algorithm as the general path (greedy descent,
+ * verdict shortcut, sorted warm starts, closed-form walks); anything else
+ * returns ST_ESCALATE and the general stages take the set. */
+
+/* least fixed point on a fixed scale; -1 = None, -2 = iteration cap */
+template <class TM>
+RT_NI double lfp_fast(const TM &tm, const TaskRec *tr, const double *views, int k, int kind, int lg,
+                      int PM, int half, int stride, double base, double start, double bound) {
+    if (base > bound) return -1.0;
+    const i64 prio_k = tr[k].prio;
+    double r = start;
+    for (int it = 0; it < ITER_CAP; it++) {
+        typename TM::template Acc<double> acc;
+        tm.acc_init(acc);
+        if (r > 0)
+            for (int i0 = 0; i0 < k; i0 += (32 >> lg)) {
+                tm.group_max_round(lg, [&](int slot, double &w, double &rr, bool &es) {
+                    int i = i0 + (slot >> lg), h = slot & ((1 << lg) - 1);
+                    if (i < k) {
+                        const TaskRec &ti = tr[i];
+                        int p = kind == K_CPU ? ti.m : ti.p;
+                        if (h < p && ti.prio < prio_k)
+                            w = walk(views + (size_t)i * stride, PM, half, p, h, r, rr, es);
+                    }
+                }, acc);
+            }
+        double I, rho;
+        bool err;
+        tm.acc_finish(lg, acc, I, rho, err);
+        if (err) return -1.0;
+        double nxt = base + I;
+        if (nxt <= r) return r;
+        nxt += rho;
+        if (nxt > bound) return -1.0;
+        r = nxt;
+    }
+    return -2.0;
+}
+
+template <class TM>
+RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
+    typedef double V;
+    typedef i64 Qt;
+    const i64 *h = c.blob;
+    const int n = (int)h[0], GN = (int)h[1];
+    const i64 A = h[3];
+    c.n = n;
+    c.GN = GN;
+    c.mm = (int)h[2];
+    c.A = A;
+    c.single_seg = 0;
+    c.vn = 0;
+    c.vq = 0;
+    c.esc = 0;
+    c.evals = 0;
+    if (n < 1 || n > c.maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > 64)
+        return ST_ESCALATE;
+    TaskRec *tr = c.TR();
+    tm.pfor(n, [&](int i) {
+        i128 vb;
+        load_task(c, i, &vb);
+        tr[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
+    });
+    i64 vb_max = 0, need = 0;
+    for (int k = 0; k < n; k++)
+        if (tr[k].flags & (TF_UNSUP | TF_IRREG)) return ST_ESCALATE;
+    for (int k = 0; k < n; k++) {
+        const TaskRec &t = tr[k];
+        if (t.flags & TF_INV) return ST_ESCALATE;             /* the reference raises */
+        if (t.flags & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE; /* first such task in order */
+        vb_max = tmax(vb_max, t.B);
+        if (t.isgpu) need += t.gmin;
+    }
+    if (need > GN) return RTGPU_UNSCHEDULABLE;
+    /* one scale for the whole search: 2 * A * lcm(1..GN), if it fits */
+    const i128 vb = (i128)vb_max * (n + 2 * RTGPU_MAX_M + 4);
+    if (vb > (i128)Num<V>::limit()) return ST_ESCALATE;
+    const Qt qlim = Num<V>::limit() / (Qt)vb;
+    Qt L = 1;
+    for (int g = 2; g <= GN; g++) {
+        L = lcm_lim<Qt>(L, (Qt)g, qlim);
+        if (L == 0) return ST_ESCALATE;
+    }
+    if (L > qlim / (2 * A)) return ST_ESCALATE;
+    const Qt q = L * 2 * A;
+    c.Vb = (i64)vb;
+    c.qlim = qlim;
+    c.fixed_q = q;
+    c.vq = q;
+    tm.sync();
+    tm.pfor(n, [&](int k) {
+        i64 b = 0;
+        for (int i = 0; i < n; i++)
+            if (tr[i].prio > tr[k].prio) b = tmax(b, tr[i].maxMlu);
+        tr[k].B = b;
+    });
+    const int lgC = c.lgC, lgM = c.lgM, halfC = c.halfC, halfM = c.halfM;
+    const int SC = c.L.SC, SM = c.L.SM, MC = c.MC, MP = c.MP;
+    V *vc = c.VC(), *vm = c.VM();
+    V *bases = c.SCR();
+    V *outs = c.SCR() + (c.MP + c.MC + 2);
+    int *ord = (int *)(c.SCR() + c.L.scr_n) - 32;
+    i64 used = 0, rest_min = need;
+    for (int k = 0; k < n; k++) {
+        const TaskRec &t = tr[k];
+        /* views of tasks before k (their counts are final) */
+        if (k > 0) tm.pfor(1, [&](int) { build_view(c, k - 1, q); });
+        const i64 *sg = c.blob + t.seg;
+        const i64 *cl_hi = sg + t.m, *ml_hi = sg + 2 * t.m + t.p;
+        const V D = Num<V>::sc(t.D, q);
+        int glo = 0, ghi = 0;
+        if (t.isgpu) {
+            rest_min -= t.gmin;
+            const i64 gmax = GN - used - rest_min;
+            if (gmax < t.gmin) return RTGPU_UNSCHEDULABLE;
+            glo = t.gmin;
+            ghi = (int)gmax;
+        }
+        /* ---- g-independent part: memory responses (Lemma 6) */
+        V sum_mr = 0, mr_ub = 0;
+        bool have_exact_mr = t.p == 0;
+        if (t.p > 0) {
+            i64 bmax_t = 0, bsum_t = 0;
+            for (int j = 0; j < t.p; j++) {
+                bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
+                bsum_t += ml_hi[j] + t.B;
+            }
+            const V bmax = Num<V>::sc(bmax_t, q);
+            const V rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, bmax, D);
+            if (rmax == -2.0) return ST_ESCALATE;
+            if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
+            mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
+        }
+        V sum_cr = -1; /* not computed yet; -2: some CR is None */
+        /* task k passes at count g?  (R2 with the MR upper bound, then exact) */
+        auto passes = [&](int g) -> int {
+            const V grup = t.isgpu ? (V)t.sInfl * (V)(q / (2 * A * (Qt)g)) + Num<V>::sc(t.sGL, q) : (V)0;
+            const V cl = Num<V>::sc(t.sClu, q);
+            if (t.p > 0 || !have_exact_mr) {
+                const V b2 = grup + mr_ub + cl;
+                const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
+                if (r == -2.0) return -1;
+                if (r >= 0) return 1;
+                if (!have_exact_mr) {
+                    /* exact memory responses, ascending bases with warm starts */
+                    tm.pfor(t.p, [&](int j) { bases[j] = Num<V>::sc(ml_hi[j] + t.B, q); });
+                    tm.pfor(t.p, [&](int j) {
+                        int rk = 0;
+                        for (int x = 0; x < t.p; x++)
+                            rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
+                        ord[rk] = j;
+                    });
+                    V pb = 0, pr = 0, acc = 0;
+                    for (int st = 0; st < t.p; st++) {
+                        const V b = bases[ord[st]];
+                        const V r0 = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, b,
+                                              st ? tmax(b, pr + (b - pb)) : b, D);
+                        if (r0 < 0) return r0 == -2.0 ? -1 : 0; /* cannot be None: rmax was not */
+                        acc += r0;
+                        pb = b;
+                        pr = r0;
+                    }
+                    sum_mr = acc;
+                    have_exact_mr = true;
+                }
+                if (sum_mr != mr_ub) {
+                    const V b3 = grup + sum_mr + cl;
+                    const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
+                    if (r3 == -2.0) return -1;
+                    if (r3 >= 0) return 1;
+                }
+            } else {
+                const V b3 = grup + cl;
+                const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
+                if (r3 == -2.0) return -1;
+                if (r3 >= 0) return 1;
+            }
+            /* R1 = GR up + sum MR + sum CR (analysis.py:207) */
+            if (sum_cr == -1) {
+                tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q); });
+                tm.pfor(t.m, [&](int j) {
+                    int rk = 0;
+                    for (int x = 0; x < t.m; x++)
+                        rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
+                    ord[rk] = j;
+                });
+                V pb = 0, pr = 0, acc = 0;
+                for (int st = 0; st < t.m; st++) {
+                    const V b = bases[ord[st]];
+                    const V r0 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b,
+                                          st ? tmax(b, pr + (b - pb)) : b, D);
+                    if (r0 == -2.0) return -1;
+                    if (r0 < 0) {
+                        acc = -2;
+                        break;
+                    }
+                    acc += r0;
+                    pb = b;
+                    pr = r0;
+                }
+                sum_cr = acc;
+            }
+            if (sum_cr < 0) return 0;
+            return grup + sum_mr + sum_cr <= D ? 1 : 0;
+        };
+        (void)outs;
+        c.evals++;
+        if (!t.isgpu) {
+            int ok = passes(0);
+            if (ok < 0) return ST_ESCALATE;
+            if (!ok) return RTGPU_UNSCHEDULABLE;
+            continue;
+        }
+        int ok = passes(glo);
+        if (ok < 0) return ST_ESCALATE;
+        int g = glo;
+        if (!ok) {
+            if (glo >= ghi) return RTGPU_UNSCHEDULABLE;
+            ok = passes(ghi);
+            if (ok < 0) return ST_ESCALATE;
+            if (!ok) return RTGPU_UNSCHEDULABLE;
+            int lo = glo, hi = ghi;
+            while (hi - lo > 1) {
+                int mid = lo + (hi - lo) / 2;
+                int o = passes(mid);
+                if (o < 0) return ST_ESCALATE;
+                if (o) hi = mid;
+                else lo = mid;
+            }
+            g = hi;
+        }
+        tm.sync();
+        if (tm.leader()) tr[k].g = g;
+        tm.sync();
+        used += g;
+    }
+    tm.pfor(n, [&](int i) { vsm_out[i] = tr[i].isgpu ? 2 * tr[i].g : 0; });
+    return RTGPU_SCHEDULABLE;
+}
+
 /* ------------------------------------------------------------ point queries */
 
 /* One query of include/rtgpu.h rtgpu_query_*: a building block of the
@@ -1577,11 +1847,13 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
     c.Vb = (i64)vb;
     c.qlim = (Qt)(Num<V>::limit() / (Qt)c.Vb);
     c.fixed_q = 0;
+#ifndef RTGPU_NO_FIXED_Q
     if (c.method == RTGPU_METHOD_RTGPU && c.GN >= 1 && c.GN <= 64) {
         Qt L = 1;
         for (int g = 2; g <= c.GN && L != 0; g++) L = lcm_lim<Qt>(L, (Qt)g, c.qlim);
         if (L != 0 && L <= c.qlim / (2 * (Qt)c.A)) c.fixed_q = L * 2 * (Qt)c.A;
     }
+#endif
     tm.sync();
     /* mem blocking term of analysis.py:162: longest copy of any lower-priority task */
     tm.pfor(c.n, [&](int k) {

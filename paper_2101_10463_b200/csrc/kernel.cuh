@@ -1,7 +1,14 @@
 /*
- * kernel.cuh -- the persistent warp-per-set kernel and its launcher,
+ * kernel.cuh -- persistent warp-per-set kernels and their launchers,
  * instantiated once per arithmetic in rtgpu_k_{f64,i64,i128}.cu (separate
- * translation units so the three instantiations compile in parallel).
+ * translation units so the instantiations compile in parallel).
+ *
+ * Stages (one stream, no host round trip; each stage reads the sets the
+ * previous one escalated from a device-side list):
+ *   0  front_kernel        FP64  every set: verdict fast path or general path
+ *   1  analyze_kernel<f64> FP64  general path
+ *   2  analyze_kernel<i64> int64
+ *   3  analyze_kernel<i128> int128 (beyond: RTGPU_RANGE)
  */
 #pragma once
 #include <cuda_runtime.h>
@@ -23,10 +30,14 @@ struct KParams {
     i64 *evals;
     int32_t *vsm;
     i64 *e2e, *den, *detail;
-    unsigned long long *ctr; /* [0..2] work counters, [3..4] escalation counts */
-    i64 *esc0, *esc1;        /* escalation lists (stage 0 -> 1, 1 -> 2) */
-    i64 set_base;            /* stage 0: first set of this launch (chunked e2e path) */
-    unsigned long long *wctr0; /* stage 0: this launch's work counter */
+    /* ctr[0] front-stage work counter (unchunked launch), ctr[1..3]
+     * general-stage work counters, ctr[4..6] lengths of esc[0..2]; esc[s]
+     * holds the sets stage s hands to stage s+1 */
+    unsigned long long *ctr;
+    i64 *esc[3];
+    int use_fast;              /* front stage runs the verdict fast path */
+    i64 set_base;              /* front stage: first set of this launch (chunked e2e path) */
+    unsigned long long *wctr0; /* front stage: this launch's work counter */
 };
 
 /* minimum resident CTAs per SM the register allocation must allow */
@@ -37,34 +48,40 @@ template <class V> struct MinBlocks { static constexpr int value = RTGPU_MINB; }
 template <> struct MinBlocks<i128> { static constexpr int value = 2; };
 
 template <class V>
-__global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KParams p, int stage) {
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    Layout<V> L;
-    L.init(p.dims);
-    SetCtx<V> c;
+__device__ __forceinline__ void kernel_ctx(SetCtx<V> &c, const Dims &dims, const Layout<V> &L, int warp) {
     c.hbase = nullptr;
     c.o_tr = warp * L.bytes;
     c.o_vc = c.o_tr + L.off_views_c;
     c.o_vm = c.o_tr + L.off_views_m;
     c.o_scr = c.o_tr + L.off_scr;
     c.L = L;
-    c.maxn = p.dims.maxn;
-    c.MC = p.dims.MC;
-    c.MP = p.dims.MP;
+    c.maxn = dims.maxn;
+    c.MC = dims.MC;
+    c.MP = dims.MP;
     set_groups(c);
+}
+
+/* Stages 1..3 (V = double, int64, int128): the general path over the sets
+ * the previous stage escalated. */
+template <class V>
+__global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KParams p, int stage) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    Layout<V> L;
+    L.init(p.dims);
+    SetCtx<V> c;
+    kernel_ctx(c, p.dims, L, warp);
     c.budget = p.budget;
     c.method = p.method;
     WarpTeam tm{lane};
-    const i64 count = stage == 0 ? p.n_sets : (i64)(stage == 1 ? p.ctr[3] : p.ctr[4]);
-    const i64 *list = stage == 0 ? nullptr : (stage == 1 ? p.esc0 : p.esc1);
-    unsigned long long *wctr = stage == 0 ? p.wctr0 : &p.ctr[stage];
+    const i64 count = (i64)p.ctr[4 + stage - 1];
+    const i64 *list = p.esc[stage - 1];
     for (;;) {
         unsigned long long idx = 0;
-        if (lane == 0) idx = atomicAdd(wctr, 1ull);
+        if (lane == 0) idx = atomicAdd(&p.ctr[stage], 1ull);
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if ((i64)idx >= count) break;
-        const i64 s = list ? list[idx] : p.set_base + (i64)idx;
+        const i64 s = list[idx];
         c.blob = p.blobs + p.set_off[s];
         const i64 tb = p.task_base[s];
         OutPtrs<V> o;
@@ -72,14 +89,14 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
         o.e2e = p.e2e + tb;
         o.den = p.den + tb;
         o.detail = p.detail ? p.detail + p.set_off[s] : nullptr;
-        const bool force = (stage == 0 && (p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) ||
-                           (stage == 1 && (p.flags & RTGPU_F_FIRST_I128));
+        const bool force = (stage == 1 && (p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) ||
+                           (stage == 2 && (p.flags & RTGPU_F_FIRST_I128));
         int st = force ? (int)ST_ESCALATE : analyze_set(tm, c, p.flags, o);
         if (st == ST_ESCALATE) {
-            if (stage < 2) {
+            if (stage < 3) {
                 if (lane == 0) {
-                    unsigned long long pos = atomicAdd(&p.ctr[3 + stage], 1ull);
-                    (stage == 0 ? p.esc0 : p.esc1)[pos] = s;
+                    unsigned long long pos = atomicAdd(&p.ctr[4 + stage], 1ull);
+                    p.esc[stage][pos] = s;
                 }
                 __syncwarp();
                 continue;
@@ -94,6 +111,56 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
     }
 }
 
+#ifdef RTGPU_FRONT_TU /* defined only in rtgpu_k_f64.cu */
+/* Stage 0: sets [set_base, set_base + n_sets) in FP64 -- the verdict fast
+ * path when it applies (RTGPU, verdict only), else the general path. */
+__global__ void __launch_bounds__(256, MinBlocks<double>::value) front_kernel(KParams p) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    Layout<double> L;
+    L.init(p.dims);
+    SetCtx<double> c;
+    kernel_ctx(c, p.dims, L, warp);
+    c.budget = p.budget;
+    c.method = p.method;
+    WarpTeam tm{lane};
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(p.wctr0, 1ull);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if ((i64)idx >= p.n_sets) break;
+        const i64 s = p.set_base + (i64)idx;
+        c.blob = p.blobs + p.set_off[s];
+        const i64 tb = p.task_base[s];
+        int st;
+        if (p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128)) {
+            st = ST_ESCALATE;
+        } else if (p.use_fast) {
+            st = fast_verdict(tm, c, p.vsm + tb);
+        } else {
+            OutPtrs<double> o;
+            o.vsm = p.vsm + tb;
+            o.e2e = p.e2e + tb;
+            o.den = p.den + tb;
+            o.detail = p.detail ? p.detail + p.set_off[s] : nullptr;
+            st = analyze_set(tm, c, p.flags, o);
+        }
+        if (st == ST_ESCALATE) {
+            if (lane == 0) {
+                unsigned long long pos = atomicAdd(&p.ctr[4], 1ull);
+                p.esc[0][pos] = s;
+            }
+            __syncwarp();
+            continue;
+        }
+        if (lane == 0) {
+            p.status[s] = st;
+            p.evals[s] = c.evals;
+        }
+        __syncwarp();
+    }
+}
+#endif
 
 /* ------------------------------------------------------------ point queries */
 
@@ -181,14 +248,11 @@ template <class V> inline int warps_per_block(const Dims &d, int *bytes_out) {
     return (size_t)L.bytes * wpb > 220 * 1024 ? 0 : wpb;
 }
 
-template <class V> inline int launch_stage(const KParams &p, int stage, cudaStream_t st) {
-    int bytes = 0;
-    int wpb = warps_per_block<V>(p.dims, &bytes);
-    if (wpb == 0) {
-        set_err_msg("task sets too large for shared memory");
-        return -3;
-    }
-    cudaError_t e = cudaFuncSetAttribute(analyze_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+template <class K> inline int launch_persistent(K kernel, const Dims &dims, int wpb_bytes_for, i64 want,
+                                                int wpb, int bytes, cudaStream_t st, const char *name,
+                                                const KParams &p, int stage, bool front) {
+    (void)wpb_bytes_for;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) {
         set_err("cudaFuncSetAttribute", e);
         return -4;
@@ -196,22 +260,50 @@ template <class V> inline int launch_stage(const KParams &p, int stage, cudaStre
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, analyze_kernel<V>, 32 * wpb, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 32 * wpb, bytes);
     if (per_sm < 1) per_sm = 1;
-    i64 need = stage == 0 ? (p.n_sets + wpb - 1) / wpb : (i64)sms * per_sm;
     i64 grid = (i64)sms * per_sm;
-    if (stage == 0 && need < grid) grid = need;
+    if (want >= 0 && want < grid) grid = want;
     if (grid < 1) grid = 1;
-    analyze_kernel<V><<<(unsigned)grid, 32 * wpb, bytes, st>>>(p, stage);
+    if (front) ((void (*)(KParams))kernel)<<<(unsigned)grid, 32 * wpb, bytes, st>>>(p);
+    else ((void (*)(KParams, int))kernel)<<<(unsigned)grid, 32 * wpb, bytes, st>>>(p, stage);
     count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) {
-        set_err("analyze_kernel launch", e);
+        set_err(name, e);
         return -5;
     }
     return 0;
 }
 
+template <class V> inline int launch_stage(const KParams &p, int stage, cudaStream_t st) {
+    int bytes = 0;
+    int wpb = warps_per_block<V>(p.dims, &bytes);
+    if (wpb == 0) {
+        set_err_msg("task sets too large for shared memory");
+        return -3;
+    }
+    /* the list length is only known on the device: a persistent grid of
+     * two CTAs per SM (escalations are few) */
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return launch_persistent((void *)analyze_kernel<V>, p.dims, 0, (i64)sms * 2, wpb, bytes, st,
+                             "analyze_kernel launch", p, stage, false);
+}
+
+#ifdef RTGPU_FRONT_TU
+inline int launch_front(const KParams &p, cudaStream_t st) {
+    int bytes = 0;
+    int wpb = warps_per_block<double>(p.dims, &bytes);
+    if (wpb == 0) {
+        set_err_msg("task sets too large for shared memory");
+        return -3;
+    }
+    return launch_persistent((void *)front_kernel, p.dims, 0, (p.n_sets + wpb - 1) / wpb, wpb, bytes,
+                             st, "front_kernel launch", p, 0, true);
+}
+#endif
 
 template <class V> inline int launch_query_stage(const QParams &p, int stage, cudaStream_t st) {
     int bytes = 0;
@@ -241,6 +333,7 @@ template <class V> inline int launch_query_stage(const QParams &p, int stage, cu
 int launch_query_f64(const QParams &p, int stage, cudaStream_t st);
 int launch_query_i64(const QParams &p, int stage, cudaStream_t st);
 int launch_query_i128(const QParams &p, int stage, cudaStream_t st);
+int launch_front_f64(const KParams &p, cudaStream_t st);
 int launch_stage_f64(const KParams &p, int stage, cudaStream_t st);
 int launch_stage_i64(const KParams &p, int stage, cudaStream_t st);
 int launch_stage_i128(const KParams &p, int stage, cudaStream_t st);

@@ -96,7 +96,7 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     }
     g_launches = 0;
     if (n_sets <= 0) return 0;
-    size_t need = CTR_WORDS * sizeof(unsigned long long) + 2 * sizeof(i64) * (size_t)n_sets;
+    size_t need = CTR_WORDS * sizeof(unsigned long long) + 3 * sizeof(i64) * (size_t)n_sets;
     if (!g_scratch.ensure(need)) {
         set_err("cudaMalloc scratch", cudaGetLastError());
         return -6;
@@ -119,10 +119,12 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     p.den = d_den;
     p.detail = d_detail;
     p.ctr = (unsigned long long *)g_scratch.p;
-    p.esc0 = (i64 *)((char *)g_scratch.p + CTR_WORDS * sizeof(unsigned long long));
-    p.esc1 = p.esc0 + n_sets;
+    p.esc[0] = (i64 *)((char *)g_scratch.p + CTR_WORDS * sizeof(unsigned long long));
+    p.esc[1] = p.esc[0] + n_sets;
+    p.esc[2] = p.esc[1] + n_sets;
     p.set_base = 0;
     p.wctr0 = &p.ctr[0];
+    p.use_fast = flags == 0 && method == RTGPU_METHOD_RTGPU;
     cudaError_t e = cudaMemsetAsync(p.ctr, 0, CTR_WORDS * sizeof(unsigned long long), st);
     if (e != cudaSuccess) {
         set_err("cudaMemsetAsync", e);
@@ -133,11 +135,12 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
         g_ev_init = true;
     }
     if (g_timing) cudaEventRecord(g_ev[0], st);
-    int rc = launch_stage_f64(p, 0, st);
+    int rc = launch_front_f64(p, st);
     if (g_timing) cudaEventRecord(g_ev[1], st);
-    if (!rc) rc = launch_stage_i64(p, 1, st);
+    if (!rc) rc = launch_stage_f64(p, 1, st);
+    if (!rc) rc = launch_stage_i64(p, 2, st);
     if (g_timing) cudaEventRecord(g_ev[2], st);
-    if (!rc) rc = launch_stage_i128(p, 2, st);
+    if (!rc) rc = launch_stage_i128(p, 3, st);
     if (g_timing) cudaEventRecord(g_ev[3], st);
     g_ev_valid = g_timing && !rc;
     g_last_ctr = p.ctr;
@@ -169,11 +172,11 @@ int rtgpu_last_stage_ms(float *ms3, int64_t *sets3) {
         cudaEventElapsedTime(&ms3[i], g_ev[i], g_ev[i + 1]);
     }
     if (sets3) {
-        unsigned long long c[5] = {0, 0, 0, 0, 0};
+        unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpy(c, g_last_ctr, sizeof c, cudaMemcpyDeviceToHost);
         sets3[0] = g_last_n;
-        sets3[1] = (int64_t)c[3];
-        sets3[2] = (int64_t)c[4];
+        sets3[1] = (int64_t)c[4];
+        sets3[2] = (int64_t)c[5] + (int64_t)c[6];
     }
     return 0;
 }
@@ -289,7 +292,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         !g_h_tb.ensure((n_sets + 1) * 8) || !g_h_status.ensure(n_sets * 4) ||
         !g_h_evals.ensure(n_sets * 8) || !g_h_vsm.ensure(T * 4) || !g_h_e2e.ensure(T * 8) ||
         !g_h_den.ensure(T * 8) || (detail && !g_h_detail.ensure(W * 8)) ||
-        !g_scratch.ensure(CTR_WORDS * 8 + 2 * 8 * (size_t)n_sets)) {
+        !g_scratch.ensure(CTR_WORDS * 8 + 3 * 8 * (size_t)n_sets)) {
         set_err("cudaMalloc", cudaGetLastError());
         return -6;
     }
@@ -319,8 +322,10 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
     p.den = (i64 *)g_h_den.p;
     p.detail = detail ? (i64 *)g_h_detail.p : nullptr;
     p.ctr = (unsigned long long *)g_scratch.p;
-    p.esc0 = (i64 *)((char *)g_scratch.p + CTR_WORDS * 8);
-    p.esc1 = p.esc0 + n_sets;
+    p.esc[0] = (i64 *)((char *)g_scratch.p + CTR_WORDS * 8);
+    p.esc[1] = p.esc[0] + n_sets;
+    p.esc[2] = p.esc[1] + n_sets;
+    p.use_fast = flags == 0 && method == RTGPU_METHOD_RTGPU;
     const int chunks = (int)std::min<i64>(MAX_CHUNKS, std::max<i64>(1, n_sets / 4096));
     cudaStream_t cp = g_s_copy;
     cudaMemsetAsync(p.ctr, 0, CTR_WORDS * 8, cp);
@@ -338,7 +343,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         q.set_base = a;
         q.n_sets = b - a;
         q.wctr0 = &p.ctr[8 + c];
-        rc = launch_stage_f64(q, 0, cs);
+        rc = launch_front_f64(q, cs);
     }
     if (rc) return rc;
     /* escalation stages and results on compute stream 0 after every chunk */
@@ -346,8 +351,9 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
     cudaStreamWaitEvent(g_s_comp[0], g_ev_comp[1], 0);
     cudaStream_t st = g_s_comp[0];
     p.n_sets = n_sets;
-    rc = launch_stage_i64(p, 1, st);
-    if (!rc) rc = launch_stage_i128(p, 2, st);
+    rc = launch_stage_f64(p, 1, st);
+    if (!rc) rc = launch_stage_i64(p, 2, st);
+    if (!rc) rc = launch_stage_i128(p, 3, st);
     if (rc) return rc;
     cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, st);

@@ -67,6 +67,35 @@ extern "C" int host_analyze_batch(const int64_t *blobs, const int64_t *set_off,
         int64_t tb = task_base[s];
         int st = ST_ESCALATE;
         int stage = first_stage;
+        if (flags == 0 && method == RTGPU_METHOD_RTGPU && first_stage == 0) {
+            /* the kernels' front stage: verdict fast path */
+            Layout<double> L;
+            L.init(d);
+            std::vector<unsigned char> slab((size_t)L.bytes + 64);
+            unsigned char *base = (unsigned char *)(((uintptr_t)slab.data() + 15) & ~(uintptr_t)15);
+            SetCtx<double> c;
+            c.blob = blob;
+            c.hbase = base;
+            c.o_tr = 0;
+            c.o_vc = L.off_views_c;
+            c.o_vm = L.off_views_m;
+            c.o_scr = L.off_scr;
+            c.L = L;
+            c.maxn = d.maxn;
+            c.MC = d.MC;
+            c.MP = d.MP;
+            set_groups(c);
+            c.budget = budget > 0 ? budget : (i64)1 << 22;
+            c.method = method;
+            SeqTeam tm;
+            st = fast_verdict(tm, c, vsm + tb);
+            evals[s] = c.evals;
+            if (st != ST_ESCALATE) {
+                status[s] = st;
+                if (stage_used) stage_used[s] = -1;
+                continue;
+            }
+        }
         for (; stage < 3 && st == ST_ESCALATE; stage++) {
             i64 ev = 0;
             if (stage == 0) {

@@ -142,3 +142,20 @@ def test_e2e_chunked_path_equals_device_path():
     assert _native.last_launch_count() > 3
     assert np.array_equal(g.status, h.status) and np.array_equal(g.vsm, h.vsm)
     assert np.array_equal(g.e2e_num, h.e2e_num) and np.array_equal(g.den, h.den)
+
+
+@pytest.mark.parametrize("u", ["1/10", "3/10", "1/2", "7/10", "1"])
+def test_gpu_verdict_fast_path_matches_oracle(u):
+    """The benchmark's mode: flags = 0 (verdict + allocation), front-stage
+    fast path, on the benchmark's own shape and seeds."""
+    gp = _native.gen_params_c(8, 5, (1000, 20000), (1000, 20000), (250, 5000), Fraction(u), 0,
+                              10, Fraction(12, 100), Fraction(1))
+    b, so, tb = _native.generate(gp, [f"1000:{u}:{i}" for i in range(2000)])
+    o = oracle.analyze_batch(b, so, tb, flags=0, threads=16, detail=False)
+    batch = DeviceBatch(b, so, tb)
+    out = batch.alloc_results()
+    batch.run(out, flags=0)
+    g = out.to_host()
+    assert np.array_equal(o["status"], g.status)
+    sched = np.repeat(o["status"] == 1, 8)
+    assert np.array_equal(o["vsm"][sched], g.vsm[sched])
