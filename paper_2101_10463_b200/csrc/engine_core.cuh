@@ -200,6 +200,18 @@ struct Dims {
     int maxn, MC, MP;
 };
 
+/* Range factor: every intermediate of an evaluation is a sum of at most
+ * max(n + 2, p + m + 1, 2p + 3) terms each bounded by the per-set
+ * max(D + T + sum of segments): interference sums (n), R1 = GR + sum MR +
+ * sum CR (p + m + 1), the verdict shortcut's MR upper bound and R2 base
+ * (2p + 3); walks and views stay below 2 max(D + T + sums). */
+RT_HD int range_factor(int n, int MC, int MP) {
+    int f = n + 4;
+    if (MP + MC + 4 > f) f = MP + MC + 4;
+    if (2 * MP + 4 > f) f = 2 * MP + 4;
+    return f;
+}
+
 template <class V> struct Layout {
     int SC, SM;        /* view stride (in V) per task for CPU / memory chains */
     int off_views_c;   /* byte offsets inside the slab */
@@ -1448,18 +1460,18 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
  * returns ST_ESCALATE and the general stages take the set. */
 
 /* least fixed point on a fixed scale; -1 = None, -2 = iteration cap */
-template <class TM>
-RT_NI double lfp_fast(const TM &tm, const TaskRec *tr, const double *views, int k, int kind, int lg,
-                      int PM, int half, int stride, double base, double start, double bound) {
-    if (base > bound) return -1.0;
+template <class V, class TM>
+RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kind, int lg,
+                 int PM, int half, int stride, V base, V start, V bound) {
+    if (base > bound) return (V)-1;
     const i64 prio_k = tr[k].prio;
-    double r = start;
+    V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
-        typename TM::template Acc<double> acc;
+        typename TM::template Acc<V> acc;
         tm.acc_init(acc);
         if (r > 0)
             for (int i0 = 0; i0 < k; i0 += (32 >> lg)) {
-                tm.group_max_round(lg, [&](int slot, double &w, double &rr, bool &es) {
+                tm.group_max_round(lg, [&](int slot, V &w, V &rr, bool &es) {
                     int i = i0 + (slot >> lg), h = slot & ((1 << lg) - 1);
                     if (i < k) {
                         const TaskRec &ti = tr[i];
@@ -1469,22 +1481,24 @@ RT_NI double lfp_fast(const TM &tm, const TaskRec *tr, const double *views, int 
                     }
                 }, acc);
             }
-        double I, rho;
+        V I, rho;
         bool err;
         tm.acc_finish(lg, acc, I, rho, err);
-        if (err) return -1.0;
-        double nxt = base + I;
+        if (err) return (V)-1;
+        V nxt = base + I;
         if (nxt <= r) return r;
         nxt += rho;
-        if (nxt > bound) return -1.0;
+        if (nxt > bound) return (V)-1;
         r = nxt;
     }
-    return -2.0;
+    return (V)-2;
 }
 
-template <class TM>
-RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
-    typedef double V;
+/* ST_ESCALATE_RANGE: only the scale did not fit V (the int64 instance may) */
+enum { ST_ESCALATE_RANGE = 98 };
+
+template <class V, class TM>
+RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     typedef i64 Qt;
     const i64 *h = c.blob;
     const int n = (int)h[0], GN = (int)h[1];
@@ -1518,15 +1532,15 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
     }
     if (need > GN) return RTGPU_UNSCHEDULABLE;
     /* one scale for the whole search: 2 * A * lcm(1..GN), if it fits */
-    const i128 vb = (i128)vb_max * (n + 2 * RTGPU_MAX_M + 4);
-    if (vb > (i128)Num<V>::limit()) return ST_ESCALATE;
+    const i128 vb = (i128)vb_max * range_factor(n, c.MC, c.MP);
+    if (vb > (i128)Num<V>::limit()) return ST_ESCALATE_RANGE;
     const Qt qlim = Num<V>::limit() / (Qt)vb;
     Qt L = 1;
     for (int g = 2; g <= GN; g++) {
         L = lcm_lim<Qt>(L, (Qt)g, qlim);
-        if (L == 0) return ST_ESCALATE;
+        if (L == 0) return ST_ESCALATE_RANGE;
     }
-    if (L > qlim / (2 * A)) return ST_ESCALATE;
+    if (L > qlim / (2 * A)) return ST_ESCALATE_RANGE;
     const Qt q = L * 2 * A;
     c.Vb = (i64)vb;
     c.qlim = qlim;
@@ -1572,7 +1586,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
             }
             const V bmax = Num<V>::sc(bmax_t, q);
             const V rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, bmax, D);
-            if (rmax == -2.0) return ST_ESCALATE;
+            if (rmax == (V)-2) return ST_ESCALATE;
             if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
             mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
         }
@@ -1584,7 +1598,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
             if (t.p > 0 || !have_exact_mr) {
                 const V b2 = grup + mr_ub + cl;
                 const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
-                if (r == -2.0) return -1;
+                if (r == (V)-2) return -1;
                 if (r >= 0) return 1;
                 if (!have_exact_mr) {
                     /* exact memory responses, ascending bases with warm starts */
@@ -1600,7 +1614,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
                         const V b = bases[ord[st]];
                         const V r0 = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, b,
                                               st ? tmax(b, pr + (b - pb)) : b, D);
-                        if (r0 < 0) return r0 == -2.0 ? -1 : 0; /* cannot be None: rmax was not */
+                        if (r0 < 0) return r0 == (V)-2 ? -1 : 0; /* cannot be None: rmax was not */
                         acc += r0;
                         pb = b;
                         pr = r0;
@@ -1611,13 +1625,13 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
                 if (sum_mr != mr_ub) {
                     const V b3 = grup + sum_mr + cl;
                     const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
-                    if (r3 == -2.0) return -1;
+                    if (r3 == (V)-2) return -1;
                     if (r3 >= 0) return 1;
                 }
             } else {
                 const V b3 = grup + cl;
                 const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
-                if (r3 == -2.0) return -1;
+                if (r3 == (V)-2) return -1;
                 if (r3 >= 0) return 1;
             }
             /* R1 = GR up + sum MR + sum CR (analysis.py:207) */
@@ -1634,7 +1648,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<double> &c, int32_t *vsm_out) {
                     const V b = bases[ord[st]];
                     const V r0 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b,
                                           st ? tmax(b, pr + (b - pb)) : b, D);
-                    if (r0 == -2.0) return -1;
+                    if (r0 == (V)-2) return -1;
                     if (r0 < 0) {
                         acc = -2;
                         break;
@@ -1841,7 +1855,7 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
         if (c.TR()[k].flags & TF_IRREG) irregular = true;
     }
     if (need > c.GN) return RTGPU_UNSCHEDULABLE;
-    i128 factor = (i128)c.n + 2 * RTGPU_MAX_M + 4;
+    i128 factor = range_factor(c.n, c.MC, c.MP);
     i128 vb = vb_max * factor;
     if (vb > (i128)Num<V>::limit()) return ST_ESCALATE;
     c.Vb = (i64)vb;

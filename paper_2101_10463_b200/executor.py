@@ -126,6 +126,7 @@ class WcrtReport:
     all_within_bound: bool = False
     kernels_within_bound: bool = False
     max_ratio: float = 0.0
+    max_kernel_ratio: float = 0.0  # worst measured kernel time / its Lemma-4 bound
     horizon_us: float = 0.0
     note: str = ""
 
@@ -253,6 +254,7 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
         seg = [r.seg_max_kernel_us[j] for j in range(len(grs))]
         kern_ok = all(x <= float(b) for x, b in zip(seg, grs))
         kok = kok and kern_ok
+        out.max_kernel_ratio = max([out.max_kernel_ratio] + [x / float(b) for x, b in zip(seg, grs)])
         out.tasks.append({"task": s.id, "priority": s.priority, "sms": len(sms),
                           "jobs": int(r.jobs), "wcrt_us": round(r.max_response_us, 1),
                           "bound_us": float(bound), "ratio": round(ratio, 4),
