@@ -40,7 +40,10 @@
  *   header (RTGPU_HDR_WORDS):
  *     [0] n_tasks  [1] physical_sms (GN)  [2] mem_model (0 two_copy, 1 one_copy)
  *     [3] alpha_den (A: interleave ratio = alpha_num / A)  [4] blob words
- *     [5] max m over tasks  [6] max p over tasks  [7] 0
+ *     [5] max m over tasks  [6] max p over tasks
+ *     [7] segment word: 0 = int64; 1 = int32 (compact: segment areas hold
+ *         int32 values and seg_off counts int32 elements from the blob
+ *         start; not combinable with RTGPU_F_DETAIL)
  *   n task records (RTGPU_TASK_WORDS each), in TaskSet.by_priority() order:
  *     [0] m (CPU segments)  [1] p (memory segments)  [2] D  [3] T
  *     [4] priority  [5] seg_off (word offset of the segment area from the

@@ -58,6 +58,12 @@ int rtgpu_exec_kernel_ms(const uint32_t *mask, int nslots, int64_t items, int it
 int rtgpu_exec_kernel_ms_idle(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
                               int idle_us, float *ms_out, int32_t *blocks_out, int32_t *sms_out);
 
+/* Same, while persistent segments keep the SMs of bg_mask busy (co-runner
+ * interference of concurrent partitions: launch path, L2, power). */
+int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
+                                int idle_us, const uint32_t *bg_mask, float *ms_out,
+                                int32_t *blocks_out, int32_t *sms_out);
+
 /* Time `reps` pinned-host copies of `bytes` (to_device: H2D, else D2H). */
 int rtgpu_exec_copy_ms(int64_t bytes, int to_device, int reps, float *ms_out);
 

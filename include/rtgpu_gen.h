@@ -26,6 +26,8 @@ typedef struct {
     int32_t physical_sms;
     int64_t eps_num, eps_den;       /* launch_overhead_frac */
     int64_t lofrac_num, lofrac_den; /* lo_frac */
+    int32_t seg_int32;              /* 1: compact blobs (int32 segment areas) */
+    int32_t pad;
 } rtgpu_gen_params;
 
 /* words of one generated blob (all sets of a call have the same size) */

@@ -93,7 +93,12 @@ typedef struct {
     otask t[MAXT];
 } oset;
 
+/* int64 copy of compact (int32) segment areas */
+static __thread int64_t seg64[MAXT * (2 * MAXM + 2 * MAXP + 4 * MAXG)];
+
 static int parse_set(const int64_t *b, oset *s) {
+    const int compact = b[7] == 1;
+    int64_t used64 = 0;
     s->n = (int)b[0];
     s->gn = (int)b[1];
     s->mm = (int)b[2];
@@ -111,6 +116,13 @@ static int parse_set(const int64_t *b, oset *s) {
         t->seg_off = r[5];
         if (t->m < 1 || t->m > MAXM || t->p < 0 || t->p > MAXP) return -1;
         const int64_t *q = b + t->seg_off;
+        if (compact) {
+            const int32_t *q32 = (const int32_t *)b + t->seg_off;
+            const int words = 2 * t->m + 2 * t->p + 4 * t->g;
+            for (int j = 0; j < words; j++) seg64[used64 + j] = q32[j];
+            q = seg64 + used64;
+            used64 += words;
+        }
         t->cl_lo = q;
         t->cl_hi = q + t->m;
         t->ml_lo = q + 2 * t->m;

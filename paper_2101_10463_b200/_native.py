@@ -31,7 +31,8 @@ class GenParamsC(ctypes.Structure):
                 ("util_num", ctypes.c_int64), ("util_den", ctypes.c_int64),
                 ("mem_model", ctypes.c_int32), ("physical_sms", ctypes.c_int32),
                 ("eps_num", ctypes.c_int64), ("eps_den", ctypes.c_int64),
-                ("lofrac_num", ctypes.c_int64), ("lofrac_den", ctypes.c_int64)]
+                ("lofrac_num", ctypes.c_int64), ("lofrac_den", ctypes.c_int64),
+                ("seg_int32", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 EXPORTS = ("rtgpu_abi_version", "rtgpu_last_error", "rtgpu_device_info", "rtgpu_analyze_host",
@@ -147,12 +148,14 @@ def last_stage_ms():
 
 
 def gen_params_c(n_tasks, n_subtasks, cpu_range, gpu_range, mem_range, util, mem_model_code,
-                 physical_sms, eps, lo_frac) -> GenParamsC:
+                 physical_sms, eps, lo_frac, compact: bool = False) -> GenParamsC:
+    """compact: int32 segment areas (header word 7 = 1); not for detail runs."""
     from fractions import Fraction
     u, e, lf = Fraction(util), Fraction(eps), Fraction(lo_frac)
     return GenParamsC(n_tasks, n_subtasks, cpu_range[0], cpu_range[1], gpu_range[0], gpu_range[1],
                       mem_range[0], mem_range[1], u.numerator, u.denominator, mem_model_code,
-                      physical_sms, e.numerator, e.denominator, lf.numerator, lf.denominator)
+                      physical_sms, e.numerator, e.denominator, lf.numerator, lf.denominator,
+                      1 if compact else 0, 0)
 
 
 def generate(params: GenParamsC, seeds, n_threads: int = 0):

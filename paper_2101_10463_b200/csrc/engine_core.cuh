@@ -183,6 +183,25 @@ template <class T> RT_HD T lcm_lim(T a, T b, T lim) {
     return a1 * b;
 }
 
+/* ------------------------------------------------------------ segment access */
+
+/* A task's segment area in either blob format: int64 words (header word 7
+ * = 0) or int32 (header word 7 = 1, the compact form the generator writes;
+ * halves the bytes a batch moves over PCIe and HBM). */
+struct SegPtr {
+    const void *p;
+    int w; /* 0: int64, 1: int32 */
+    RT_HD i64 operator[](int j) const {
+        return w ? (i64)((const int32_t *)p)[j] : ((const i64 *)p)[j];
+    }
+    RT_HD SegPtr operator+(int j) const {
+        SegPtr r;
+        r.p = w ? (const void *)((const int32_t *)p + j) : (const void *)((const i64 *)p + j);
+        r.w = w;
+        return r;
+    }
+};
+
 /* ------------------------------------------------------------ per-task data */
 
 struct TaskRec {
@@ -255,6 +274,13 @@ template <class V> struct SetCtx {
     unsigned char *hbase; /* host harness only */
     int o_tr, o_vc, o_vm, o_scr;
     RT_HD unsigned char *sbase() const;
+    int segw; /* header word 7: 0 int64 segment areas, 1 int32 */
+    RT_HD SegPtr segs(i64 seg_off) const {
+        SegPtr r;
+        r.w = segw;
+        r.p = segw ? (const void *)((const int32_t *)blob + seg_off) : (const void *)(blob + seg_off);
+        return r;
+    }
     RT_HD TaskRec *TR() const { return (TaskRec *)(sbase() + o_tr); }
     RT_HD V *VC() const { return (V *)(sbase() + o_vc); }
     RT_HD V *VM() const { return (V *)(sbase() + o_vm); }
@@ -423,10 +449,10 @@ template <class V>
 RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     typedef Num<V> N;
     const TaskRec &t = c.TR()[i];
-    const i64 *sg = c.blob + t.seg;
+    const SegPtr sg = c.segs(t.seg);
     const int m = t.m, p = t.p, g = m - 1;
-    const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
-    const i64 *gw_lo = ml_hi + p;
+    const SegPtr cl_lo = sg, cl_hi = sg + m, ml_lo = sg + 2 * m, ml_hi = ml_lo + p;
+    const SegPtr gw_lo = ml_hi + p;
     typename Num<V>::Qt perlo = t.isgpu ? q / (2 * (typename Num<V>::Qt)t.g) : q;
     if (c.single_seg) {
         /* busy-waiting baseline (analysis.py:360): one execution segment of
@@ -778,8 +804,8 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
     const V D = N::sc(t.D, q);
     V *bases = c.SCR();
     V *outs = c.SCR() + (c.MP + c.MC + 2);
-    const i64 *sg = c.blob + t.seg;
-    const i64 *cl_hi = sg + t.m, *ml_hi = sg + 2 * t.m + t.p;
+    const SegPtr sg = c.segs(t.seg);
+    const SegPtr cl_hi = sg + t.m, ml_hi = sg + 2 * t.m + t.p;
     /* memory segments: analysis.py:156 (blocking = longest lp copy) */
     V sum_mr = 0;
     bool mr_none = false;
@@ -875,10 +901,10 @@ RT_NI void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
         *vb_out = 0;
         return;
     }
-    const i64 *sg = c.blob + t.seg;
-    const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
+    const SegPtr sg = c.segs(t.seg);
+    const SegPtr cl_lo = sg, cl_hi = sg + m, ml_lo = sg + 2 * m, ml_hi = ml_lo + p;
     const int g = m - 1;
-    const i64 *gw_lo = ml_hi + p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+    const SegPtr gw_lo = ml_hi + p, gw_hi = gw_lo + g, gl = gw_hi + g, an = gl + g;
     i128 tot = 0;
     t.sClu = t.sCll = t.sMlu = t.sMll = t.sGWlo = t.sInfl = t.sGL = t.innerCll = t.maxMlu = 0;
     bool neg = false;
@@ -968,9 +994,9 @@ RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool sto
         eval_task(tm, c, k, t.g, lcm_pre, true, res, mr, cr);
         if (c.esc || c.stuck) return false;
         const Qt q = res.q;
-        const i64 *sg = c.blob + t.seg;
+        const SegPtr sg = c.segs(t.seg);
         const int m = t.m, p = t.p, g = m - 1;
-        const i64 *gw_lo = sg + 2 * m + 2 * p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+        const SegPtr gw_lo = sg + 2 * m + 2 * p, gw_hi = gw_lo + g, gl = gw_hi + g, an = gl + g;
         if (t.isgpu) {
             const Qt perlo = q / (2 * (Qt)t.g);
             const Qt perhi = q / (2 * (Qt)c.A * (Qt)t.g);
@@ -1194,9 +1220,9 @@ template <class V> RT_HD V grup_at(const SetCtx<V> &c, const TaskRec &t, int gco
  * self-suspension blocking a higher-priority task can suffer from it). */
 template <class V> RT_HD V max_susp_hi(const SetCtx<V> &c, const TaskRec &t, int gcount, typename Num<V>::Qt q) {
     if (!t.isgpu) return 0;
-    const i64 *sg = c.blob + t.seg;
+    const SegPtr sg = c.segs(t.seg);
     const int m = t.m, p = t.p, g = m - 1;
-    const i64 *ml_hi = sg + 2 * m + p, *gw_hi = sg + 2 * m + 2 * p + g, *gl = gw_hi + g, *an = gl + g;
+    const SegPtr ml_hi = sg + 2 * m + p, gw_hi = sg + 2 * m + 2 * p + g, gl = gw_hi + g, an = gl + g;
     typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * gcount);
     V best = 0;
     for (int j = 0; j < g; j++) {
@@ -1211,10 +1237,10 @@ template <class V> RT_HD V max_susp_hi(const SetCtx<V> &c, const TaskRec &t, int
 /* SuspTask validity (suspension.py:35) of task t under its count, exact:
  * every lo <= hi, and sum(exec hi) + sum(susp lo) <= T. */
 template <class V> RT_HD bool susp_valid(const SetCtx<V> &c, const TaskRec &t, int gcount, typename Num<V>::Qt q) {
-    const i64 *sg = c.blob + t.seg;
+    const SegPtr sg = c.segs(t.seg);
     const int m = t.m, p = t.p, g = m - 1;
-    const i64 *cl_lo = sg, *cl_hi = sg + m, *ml_lo = sg + 2 * m, *ml_hi = ml_lo + p;
-    const i64 *gw_lo = ml_hi + p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+    const SegPtr cl_lo = sg, cl_hi = sg + m, ml_lo = sg + 2 * m, ml_hi = ml_lo + p;
+    const SegPtr gw_lo = ml_hi + p, gw_hi = gw_lo + g, gl = gw_hi + g, an = gl + g;
     typename Num<V>::Qt perlo = t.isgpu ? q / (2 * (typename Num<V>::Qt)gcount) : q;
     typename Num<V>::Qt perhi =
         t.isgpu ? q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * gcount) : q;
@@ -1267,7 +1293,7 @@ RT_NI V baseline_response(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt
     if (r2 >= 0 && !want_all) return r2;
     V *bases = c.SCR();
     V *outs = c.SCR() + (c.MP + c.MC + 2);
-    const i64 *cl_hi = c.blob + t.seg + t.m;
+    const SegPtr cl_hi = c.segs(t.seg) + t.m;
     tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q) + B; });
     bool none;
     lfp_many(tm, c, k, K_CPU, bases, outs, t.m, D, true, none);
@@ -1335,9 +1361,9 @@ RT_NI int eval_alloc_baseline(const TM &tm, SetCtx<V> &c, bool want_all, const O
                 out->den[k] = (i64)q;
             }
             if (out->detail && t.isgpu) {
-                const i64 *sg = c.blob + t.seg;
+                const SegPtr sg = c.segs(t.seg);
                 const int m = t.m, p = t.p, g = m - 1;
-                const i64 *gw_lo = sg + 2 * m + 2 * p, *gw_hi = gw_lo + g, *gl = gw_hi + g, *an = gl + g;
+                const SegPtr gw_lo = sg + 2 * m + 2 * p, gw_hi = gw_lo + g, gl = gw_hi + g, an = gl + g;
                 i64 *d = out->detail + t.seg;
                 const Qt perlo = q / (2 * (Qt)t.g), perhi = q / (2 * (Qt)c.A * (Qt)t.g);
                 tm.pfor(g, [&](int j) {
@@ -1410,9 +1436,9 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
                 for (int i = 0; i < c.n; i++) {
                     const TaskRec &t = c.TR()[i];
                     if (t.prio <= c.TR()[f].prio || !t.isgpu) continue;
-                    const i64 *sg = c.blob + t.seg;
+                    const SegPtr sg = c.segs(t.seg);
                     const int m = t.m, p = t.p, g = m - 1;
-                    const i64 *ml_hi = sg + 2 * m + p, *gl = sg + 2 * m + 2 * p + 2 * g;
+                    const SegPtr ml_hi = sg + 2 * m + p, gl = sg + 2 * m + 2 * p + 2 * g;
                     for (int j = 0; j < g; j++) {
                         i64 x = c.mm == RTGPU_TWO_COPY ? ml_hi[2 * j] + ml_hi[2 * j + 1] : ml_hi[j];
                         Bmin = tmax(Bmin, Num<V>::sc(x + gl[j], q));
@@ -1507,6 +1533,8 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     c.GN = GN;
     c.mm = (int)h[2];
     c.A = A;
+    c.segw = (int)h[7];
+    if (c.segw < 0 || c.segw > 1) return ST_ESCALATE;
     c.single_seg = 0;
     c.vn = 0;
     c.vq = 0;
@@ -1564,8 +1592,8 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         const TaskRec &t = tr[k];
         /* views of tasks before k (their counts are final) */
         if (k > 0) tm.pfor(1, [&](int) { build_view(c, k - 1, q); });
-        const i64 *sg = c.blob + t.seg;
-        const i64 *cl_hi = sg + t.m, *ml_hi = sg + 2 * t.m + t.p;
+        const SegPtr sg = c.segs(t.seg);
+        const SegPtr cl_hi = sg + t.m, ml_hi = sg + 2 * t.m + t.p;
         const V D = Num<V>::sc(t.D, q);
         int glo = 0, ghi = 0;
         if (t.isgpu) {
@@ -1713,6 +1741,7 @@ RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 ho
     c.GN = (int)h[1];
     c.mm = (int)h[2];
     c.A = h[3];
+    c.segw = (int)h[7];
     c.vn = 0;
     c.vq = 0;
     c.esc = 0;
@@ -1748,7 +1777,7 @@ RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 ho
     if (q > c.qlim) return ST_ESCALATE;
     ensure_views(tm, c, c.n, q);
     const TaskRec &t = c.TR()[k];
-    const i64 *sg = c.blob + t.seg;
+    const SegPtr sg = c.segs(t.seg);
     const V D = Num<V>::sc(t.D, q);
     V r = (V)-1;
     *res_den = (i64)q;
@@ -1816,6 +1845,7 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
     c.GN = (int)h[1];
     c.mm = (int)h[2];
     c.A = h[3];
+    c.segw = (int)h[7];
     c.vn = 0;
     c.vq = 0;
     c.esc = 0;
@@ -1828,7 +1858,9 @@ RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
         o.e2e[i] = RTGPU_ABSENT;
         o.den[i] = 1;
     });
-    if (c.n < 0 || c.n > c.maxn || c.A < 1 || (c.mm != 0 && c.mm != 1)) return RTGPU_INVALID;
+    if (c.n < 0 || c.n > c.maxn || c.A < 1 || (c.mm != 0 && c.mm != 1) || c.segw < 0 ||
+        c.segw > 1 || (c.segw == 1 && o.detail))
+        return RTGPU_INVALID; /* the detail output mirrors the int64 layout */
     /* per-task loading; range bound = (n + 2M + 4) * max(D + T + sums) */
     i128 vb_max = 0;
     {

@@ -174,10 +174,29 @@ int rtgpu_exec_kernel_ms(const uint32_t *mask, int nslots, int64_t items, int it
 
 int rtgpu_exec_kernel_ms_idle(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
                               int idle_us, float *ms_out, int32_t *blocks_out, int32_t *sms_out) {
+    return rtgpu_exec_kernel_ms_loaded(mask, nslots, items, iters, reps, idle_us, nullptr, ms_out,
+                                       blocks_out, sms_out);
+}
+
+int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
+                                int idle_us, const uint32_t *bg_mask, float *ms_out,
+                                int32_t *blocks_out, int32_t *sms_out) {
     Lane L;
     if (lane_init(L, 64)) {
         strcpy(g_err, "executor allocation failed");
         return -1;
+    }
+    /* co-runner load: persistent segments on bg_mask (other partitions), kept
+     * running for the whole measurement and stopped by advancing their work
+     * counter past the end */
+    Lane B;
+    const bool loaded = bg_mask != nullptr;
+    if (loaded) {
+        if (lane_init(B, 64)) {
+            strcpy(g_err, "executor allocation failed");
+            return -1;
+        }
+        enqueue_segment(B, bg_mask, 2, (long long)1 << 40, iters, false);
     }
     /* warm up once, then time reps launches individually */
     enqueue_segment(L, mask, nslots, items, iters, false);
@@ -204,6 +223,12 @@ int rtgpu_exec_kernel_ms_idle(const uint32_t *mask, int nslots, int64_t items, i
             if (blocks_out) *blocks_out = outside ? -1 : (int)nb;
             if (sms_out) *sms_out = distinct;
         }
+    }
+    if (loaded) {
+        const unsigned long long stop = (unsigned long long)1 << 41;
+        cudaMemcpy(B.work, &stop, sizeof stop, cudaMemcpyHostToDevice);
+        cudaStreamSynchronize(B.st);
+        lane_free(B);
     }
     cudaError_t e = cudaGetLastError();
     lane_free(L);

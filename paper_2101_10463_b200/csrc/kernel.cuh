@@ -137,17 +137,9 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) front_kernel(KP
             st = ST_ESCALATE;
         } else if (p.use_fast) {
             st = fast_verdict(tm, c, p.vsm + tb);
-            if (st == ST_ESCALATE_RANGE) {
-                /* same slab layout (8-byte V): retry the fast path in int64 */
-                SetCtx<i64> ci;
-                kernel_ctx(ci, p.dims, *(const Layout<i64> *)&L, warp);
-                ci.blob = c.blob;
-                ci.budget = p.budget;
-                ci.method = p.method;
-                st = fast_verdict(tm, ci, p.vsm + tb);
-                c.evals = ci.evals;
-                if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
-            }
+            /* a scale beyond FP64: the general path's per-task scales are
+             * cheaper than an int64 fast path (measured) */
+            if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
         } else {
             OutPtrs<double> o;
             o.vsm = p.vsm + tb;

@@ -305,7 +305,8 @@ void gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
             A = A / gcd64(A, den) * den;
         }
     const int seg_words = 2 * m + 2 * pm + 4 * (m - 1);
-    const int64_t words = RTGPU_HDR_WORDS + (int64_t)n * (RTGPU_TASK_WORDS + seg_words);
+    const bool c32 = p->seg_int32 != 0;
+    const int64_t words = rtgpu_gen_blob_words(p);
     out[0] = n;
     out[1] = p->physical_sms;
     out[2] = p->mem_model;
@@ -313,8 +314,10 @@ void gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
     out[4] = words;
     out[5] = m;
     out[6] = pm;
-    out[7] = 0;
-    int64_t seg = RTGPU_HDR_WORDS + (int64_t)n * RTGPU_TASK_WORDS;
+    out[7] = c32 ? 1 : 0;
+    /* segment areas after the records; seg_off in int64 words or int32 elements */
+    int64_t seg = (RTGPU_HDR_WORDS + (int64_t)n * RTGPU_TASK_WORDS) * (c32 ? 2 : 1);
+    int32_t *out32 = (int32_t *)out;
     /* tasks in priority order (TaskSet.by_priority) */
     std::vector<int> byp(n);
     for (int i = 0; i < n; i++) byp[prio[i] - 1] = i;
@@ -329,17 +332,21 @@ void gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
         rec[5] = seg;
         rec[6] = d.idx;
         rec[7] = 0;
-        int64_t *s = out + seg;
-        int w = 0;
-        for (int j = 0; j < m; j++) s[w++] = d.cl_lo[j];
-        for (int j = 0; j < m; j++) s[w++] = d.cl_hi[j];
-        for (int j = 0; j < pm; j++) s[w++] = d.ml_lo[j];
-        for (int j = 0; j < pm; j++) s[w++] = d.ml_hi[j];
-        for (int j = 0; j < m - 1; j++) s[w++] = d.gw_lo[j];
-        for (int j = 0; j < m - 1; j++) s[w++] = d.gw_hi[j];
-        for (int j = 0; j < m - 1; j++) s[w++] = d.gl[j];
-        for (int j = 0; j < m - 1; j++) s[w++] = (int64_t)d.pct[j] * A / 100;
-        seg += w;
+        std::vector<int64_t> v;
+        v.reserve(seg_words);
+        for (int j = 0; j < m; j++) v.push_back(d.cl_lo[j]);
+        for (int j = 0; j < m; j++) v.push_back(d.cl_hi[j]);
+        for (int j = 0; j < pm; j++) v.push_back(d.ml_lo[j]);
+        for (int j = 0; j < pm; j++) v.push_back(d.ml_hi[j]);
+        for (int j = 0; j < m - 1; j++) v.push_back(d.gw_lo[j]);
+        for (int j = 0; j < m - 1; j++) v.push_back(d.gw_hi[j]);
+        for (int j = 0; j < m - 1; j++) v.push_back(d.gl[j]);
+        for (int j = 0; j < m - 1; j++) v.push_back((int64_t)d.pct[j] * A / 100);
+        for (size_t j = 0; j < v.size(); j++) {
+            if (c32) out32[seg + (int64_t)j] = (int32_t)v[j]; /* generator values < 2^31 */
+            else out[seg + (int64_t)j] = v[j];
+        }
+        seg += (int64_t)v.size();
     }
 }
 
@@ -350,7 +357,8 @@ extern "C" {
 int64_t rtgpu_gen_blob_words(const rtgpu_gen_params *p) {
     const int n = p->n_tasks, m = p->n_subtasks;
     const int pm = m < 2 ? 0 : (p->mem_model == RTGPU_ONE_COPY ? m - 1 : 2 * m - 2);
-    return RTGPU_HDR_WORDS + (int64_t)n * (RTGPU_TASK_WORDS + 2 * m + 2 * pm + 4 * (m - 1));
+    const int64_t seg = (int64_t)n * (2 * m + 2 * pm + 4 * (m - 1));
+    return RTGPU_HDR_WORDS + (int64_t)n * RTGPU_TASK_WORDS + (p->seg_int32 ? (seg + 1) / 2 : seg);
 }
 
 int rtgpu_generate(const rtgpu_gen_params *p, int64_t n_sets, const int64_t *int_seeds,
@@ -362,6 +370,8 @@ int rtgpu_generate(const rtgpu_gen_params *p, int64_t n_sets, const int64_t *int
         p->cpu_lo < 0 || p->gpu_lo < 0 || p->mem_lo < 0 || p->lofrac_den <= 0 ||
         p->lofrac_num <= 0 || p->lofrac_num > p->lofrac_den || p->eps_den <= 0)
         return -1;
+    if (p->seg_int32 && (p->cpu_hi > 0x3fffffff || p->gpu_hi > 0x3fffffff || p->mem_hi > 0x1fffffff))
+        return -1; /* segment values (and the merged copies) must fit int32 */
     const int64_t words = rtgpu_gen_blob_words(p);
     for (int64_t s = 0; s <= n_sets; s++) {
         set_off[s] = s * words;

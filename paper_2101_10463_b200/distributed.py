@@ -60,7 +60,8 @@ def sharded_sweep(cfg: SweepConfig, rank: int = 0, world: int = 1, group=None,
             for mm in cfg.mem_models:
                 cells.append((value, u, mm))
                 if seeds:
-                    parts.append(generate_blobs(dataclasses.replace(gen, mem_model=mm), seeds))
+                    parts.append(generate_blobs(dataclasses.replace(gen, mem_model=mm), seeds,
+                                                compact=True))
     local = np.zeros((len(cfg.methods), len(cells)), dtype=np.int64)
     if parts:
         blobs, set_off, task_base = concat_batches(parts)

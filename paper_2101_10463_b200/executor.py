@@ -61,6 +61,12 @@ def _lib():
                                                 ctypes.c_int, ctypes.POINTER(ctypes.c_float),
                                                 ctypes.POINTER(ctypes.c_int32),
                                                 ctypes.POINTER(ctypes.c_int32)]
+        L.rtgpu_exec_kernel_ms_loaded.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_int,
+                                                  ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_int, ctypes.POINTER(ctypes.c_uint32),
+                                                  ctypes.POINTER(ctypes.c_float),
+                                                  ctypes.POINTER(ctypes.c_int32),
+                                                  ctypes.POINTER(ctypes.c_int32)]
         L.rtgpu_exec_copy_ms.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_float)]
         L.rtgpu_exec_run.argtypes = [ctypes.POINTER(ExecTaskC), ctypes.c_int, ctypes.c_double,
@@ -75,6 +81,19 @@ def mask_of(sms) -> "ctypes.Array":
     for s in sms:
         m[s >> 5] |= 1 << (s & 31)
     return m
+
+
+def kernel_ms_loaded(sms, bg_sms, nslots: int, items: int, iters: int, reps: int = 3):
+    """Like kernel_ms while the SMs bg_sms run co-runner persistent segments."""
+    _native.require_device()
+    out = (ctypes.c_float * reps)()
+    nb, ns = ctypes.c_int32(0), ctypes.c_int32(0)
+    rc = _lib().rtgpu_exec_kernel_ms_loaded(mask_of(sms), nslots, items, iters, reps, 0,
+                                            mask_of(bg_sms), out, ctypes.byref(nb),
+                                            ctypes.byref(ns))
+    if rc:
+        raise RuntimeError(_lib().rtgpu_exec_last_error().decode())
+    return [float(x) for x in out], nb.value, ns.value
 
 
 def kernel_ms(sms, nslots: int, items: int, iters: int, reps: int = 5, idle_us: int = 0):
@@ -144,8 +163,12 @@ def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = 0.12
     idle GPU (the SM clock may have dropped; clocks are not locked here)."""
     t1, t2 = [], []
     for sm in CAL_SMS:
+        others = [x for x in range(148) if x != sm]
         t1 += kernel_ms([sm], 1, items, iters, reps)[0] + kernel_ms([sm], 1, items, iters, 2, idle_us)[0]
         t2 += kernel_ms([sm], 2, items, iters, reps)[0] + kernel_ms([sm], 2, items, iters, 2, idle_us)[0]
+        # co-runners on every other SM (the executor's concurrent partitions)
+        t1 += kernel_ms_loaded([sm], others, 1, items, iters, 2)[0]
+        t2 += kernel_ms_loaded([sm], others, 2, items, iters, 2)[0]
     t1u, t2u = max(t1) * 1e3, max(t2) * 1e3
     alpha = Fraction(max(100, min(180, math.ceil(200 * t2u / t1u))), 100)
     return KernelCal(items, iters, t1u, t2u, alpha, int(min(t1) * 1e3 * 0.95),

@@ -89,25 +89,7 @@ extern "C" int host_analyze_batch(const int64_t *blobs, const int64_t *set_off,
             c.method = method;
             SeqTeam tm;
             st = fast_verdict(tm, c, vsm + tb);
-            if (st == ST_ESCALATE_RANGE) {
-                SetCtx<i64> ci;
-                ci.blob = blob;
-                ci.hbase = base;
-                ci.o_tr = 0;
-                ci.o_vc = L.off_views_c;
-                ci.o_vm = L.off_views_m;
-                ci.o_scr = L.off_scr;
-                ci.L = *(const Layout<i64> *)&L;
-                ci.maxn = d.maxn;
-                ci.MC = d.MC;
-                ci.MP = d.MP;
-                set_groups(ci);
-                ci.budget = c.budget;
-                ci.method = method;
-                st = fast_verdict(tm, ci, vsm + tb);
-                c.evals = ci.evals;
-                if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
-            }
+            if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
             evals[s] = c.evals;
             if (st != ST_ESCALATE) {
                 status[s] = st;

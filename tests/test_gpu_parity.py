@@ -159,3 +159,20 @@ def test_gpu_verdict_fast_path_matches_oracle(u):
     assert np.array_equal(o["status"], g.status)
     sched = np.repeat(o["status"] == 1, 8)
     assert np.array_equal(o["vsm"][sched], g.vsm[sched])
+
+
+def test_gpu_compact_blobs_equal_int64_blobs():
+    """Compact (int32 segment) blobs give the same results as int64 blobs."""
+    res = []
+    for compact in (False, True):
+        gp = _native.gen_params_c(8, 5, (1000, 20000), (1000, 20000), (250, 5000), Fraction(1, 2),
+                                  0, 10, Fraction(12, 100), Fraction(1), compact=compact)
+        b, so, tb = _native.generate(gp, [f"8:{i}" for i in range(3000)])
+        batch = DeviceBatch(b, so, tb)
+        for flags in (0, F_BOUNDS):
+            out = batch.alloc_results()
+            batch.run(out, flags=flags)
+            res.append(out.to_host())
+    for a, b in ((res[0], res[2]), (res[1], res[3])):
+        assert np.array_equal(a.status, b.status) and np.array_equal(a.vsm, b.vsm)
+    assert np.array_equal(res[1].e2e_num, res[3].e2e_num) and np.array_equal(res[1].den, res[3].den)
