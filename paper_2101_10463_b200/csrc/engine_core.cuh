@@ -1485,6 +1485,107 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
  * verdict shortcut, sorted warm starts, closed-form walks); anything else
  * returns ST_ESCALATE and the general stages take the set. */
 
+/* load_task for the fast path: int64 only.  Values beyond the guarded
+ * ranges (segments >= 2^31, A >= 2^16, D or T >= 2^56) mark the task
+ * TF_UNSUP, which sends the set to the general path (128-bit load). */
+template <class V>
+RT_NI void load_task_fast(SetCtx<V> &c, int i) {
+    const i64 *r = c.blob + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
+    TaskRec &t = c.TR()[i];
+    t.m = (int)r[0];
+    t.p = (int)r[1];
+    t.D = r[2];
+    t.T = r[3];
+    t.prio = r[4];
+    t.seg = r[5];
+    t.idx = i;
+    t.flags = 0;
+    t.g = 0;
+    t.gmin = 0;
+    t.isgpu = t.m > 1;
+    const int m = t.m, p = t.p, g = m - 1;
+    const int want_p = m < 2 ? 0 : (c.mm == RTGPU_TWO_COPY ? 2 * m - 2 : m - 1);
+    const i64 big = (i64)1 << 56;
+    if (m < 1 || m > c.MC || p != want_p || p > c.MP || t.T <= 0 || t.D <= 0 || t.D > t.T ||
+        t.T >= big || c.A >= (1 << 16)) {
+        t.flags = TF_UNSUP;
+        t.B = 0;
+        return;
+    }
+    const SegPtr sg = c.segs(t.seg);
+    i64 clu = 0, cll = 0, mlu = 0, mll = 0, gwl = 0, infl = 0, gls = 0, inner = 0, mx = 0, ih = 0;
+    bool bad = false;
+    for (int j = 0; j < 2 * m + 2 * p + 4 * g; j++) {
+        const i64 v = sg[j];
+        bad = bad || v < 0 || v >= ((i64)1 << 31);
+    }
+    if (bad) {
+        t.flags = TF_UNSUP;
+        t.B = 0;
+        return;
+    }
+    for (int j = 0; j < m; j++) {
+        clu += sg[m + j];
+        cll += sg[j];
+        if (j >= 1 && j <= m - 2) inner += sg[j];
+    }
+    for (int j = 0; j < p; j++) {
+        mll += sg[2 * m + j];
+        const i64 h = sg[2 * m + p + j];
+        mlu += h;
+        mx = tmax(mx, h);
+    }
+    for (int j = 0; j < g; j++) {
+        const i64 lo = sg[2 * m + 2 * p + j], hi = sg[2 * m + 2 * p + g + j];
+        const i64 gl = sg[2 * m + 2 * p + 2 * g + j], an = sg[2 * m + 2 * p + 3 * g + j];
+        const i64 w = hi * an, o = gl * c.A; /* < 2^47 */
+        if (o > w) t.flags |= TF_INV;
+        infl += w - o;
+        ih += w;
+        gls += gl;
+        gwl += lo;
+    }
+    t.sClu = clu;
+    t.sCll = cll;
+    t.sMlu = mlu;
+    t.sMll = mll;
+    t.sGWlo = gwl;
+    t.sInfl = infl;
+    t.sGL = gls;
+    t.innerCll = inner;
+    t.maxMlu = mx;
+    /* range bound and isolated-bound minimum count (analysis.py:239) */
+    t.B = t.D + t.T + clu + cll + mlu + mll + gwl + gls + ih / c.A + 1;
+    if (t.isgpu) {
+        const i64 X = t.D - gls - mlu - clu;
+        i64 gm = 0;
+        if (c.GN >= 1) {
+            if (X > 0) {
+                if (X > ((i64)1 << 60) / (2 * c.A)) gm = 1; /* infl / (2 A X) < 1 */
+                else {
+                    const i64 den = 2 * c.A * X;
+                    gm = (infl + den - 1) / den;
+                    if (gm < 1) gm = 1;
+                }
+                if (gm > c.GN) gm = 0;
+            } else if (X == 0 && infl == 0) {
+                gm = 1;
+            }
+        }
+        if (gm == 0) t.flags |= TF_ISOFAIL;
+        t.gmin = (int)gm;
+        if (gm > 0) {
+            /* regular: no wrap-around gap negative at gm (ceil division avoids overflow) */
+            const i64 need = (gwl + 2 * gm - 1) / (2 * gm);
+            if (t.T - clu - mll < need) t.flags |= TF_IRREG;
+            if (t.T - mlu - inner < need) t.flags |= TF_IRREG;
+        }
+    } else {
+        if (clu > t.D) t.flags |= TF_ISOFAIL;
+        if (t.T - clu < 0) t.flags |= TF_IRREG;
+    }
+}
+
 /* least fixed point on a fixed scale; -1 = None, -2 = iteration cap */
 template <class V, class TM>
 RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kind, int lg,
@@ -1543,11 +1644,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     if (n < 1 || n > c.maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > 64)
         return ST_ESCALATE;
     TaskRec *tr = c.TR();
-    tm.pfor(n, [&](int i) {
-        i128 vb;
-        load_task(c, i, &vb);
-        tr[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
-    });
+    tm.pfor(n, [&](int i) { load_task_fast(c, i); });
     i64 vb_max = 0, need = 0;
     for (int k = 0; k < n; k++)
         if (tr[k].flags & (TF_UNSUP | TF_IRREG)) return ST_ESCALATE;
@@ -1692,30 +1789,42 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         };
         (void)outs;
         c.evals++;
-        if (!t.isgpu) {
-            int ok = passes(0);
-            if (ok < 0) return ST_ESCALATE;
-            if (!ok) return RTGPU_UNSCHEDULABLE;
-            continue;
-        }
-        int ok = passes(glo);
-        if (ok < 0) return ST_ESCALATE;
-        int g = glo;
-        if (!ok) {
-            if (glo >= ghi) return RTGPU_UNSCHEDULABLE;
-            ok = passes(ghi);
-            if (ok < 0) return ST_ESCALATE;
-            if (!ok) return RTGPU_UNSCHEDULABLE;
-            int lo = glo, hi = ghi;
-            while (hi - lo > 1) {
-                int mid = lo + (hi - lo) / 2;
-                int o = passes(mid);
-                if (o < 0) return ST_ESCALATE;
-                if (o) hi = mid;
-                else lo = mid;
+        /* smallest passing count: glo, else ghi, else bisection -- one call
+         * site for `passes` keeps a single inlined copy */
+        int g = 0, lo = glo, hi = ghi, phase = t.isgpu ? 0 : 3;
+        int cand = t.isgpu ? glo : 0;
+        for (;;) {
+            const int o = passes(cand);
+            if (o < 0) return ST_ESCALATE;
+            if (phase == 3) { /* pure-CPU task: one evaluation */
+                if (!o) return RTGPU_UNSCHEDULABLE;
+                break;
             }
-            g = hi;
+            if (phase == 0) {
+                if (o) {
+                    g = glo;
+                    break;
+                }
+                if (glo >= ghi) return RTGPU_UNSCHEDULABLE;
+                phase = 1;
+                cand = ghi;
+                continue;
+            }
+            if (phase == 1) {
+                if (!o) return RTGPU_UNSCHEDULABLE;
+                phase = 2;
+            } else if (o) {
+                hi = cand;
+            } else {
+                lo = cand;
+            }
+            if (hi - lo <= 1) {
+                g = hi;
+                break;
+            }
+            cand = lo + (hi - lo) / 2;
         }
+        if (!t.isgpu) continue;
         tm.sync();
         if (tm.leader()) tr[k].g = g;
         tm.sync();

@@ -140,6 +140,11 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) front_kernel(KP
             /* a scale beyond FP64: the general path's per-task scales are
              * cheaper than an int64 fast path (measured) */
             if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
+            if (st != RTGPU_SCHEDULABLE && st != ST_ESCALATE) {
+                const int n = (int)c.blob[0];
+                for (int i = lane; i < n; i += 32) p.vsm[tb + i] = 0; /* no allocation */
+                __syncwarp();
+            }
         } else {
             OutPtrs<double> o;
             o.vsm = p.vsm + tb;
