@@ -1947,7 +1947,7 @@ RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 ho
 
 /* Whole pipeline for one set; returns the status (or ST_ESCALATE). */
 template <class V, class TM>
-RT_HD int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<V> &o) {
+RT_NI int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<V> &o) {
     typedef typename Num<V>::Qt Qt;
     const i64 *h = c.blob;
     c.n = (int)h[0];
