@@ -62,14 +62,23 @@ def num(x):
         return None
 
 
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "usecond": 1e3,
+         "ms": 1e6, "msecond": 1e6, "nsecond": 1, "s": 1e9, "second": 1e9}
+
+
+def to_base(v, unit):
+    """ncu scales units per value (Mbyte, ms ...): back to bytes / ns."""
+    if v is None:
+        return None
+    return v * SCALE.get(unit, 1)
+
+
 def summarise(rep):
     d = raw(rep)
     s = {"kernel": d.get("Kernel Name", ("?", ""))[0]}
     for k, name in METRICS.items():
         if k in d:
-            s[name] = num(d[k][0])
-            if d[k][1]:
-                s[name + "_unit"] = d[k][1]
+            s[name] = to_base(num(d[k][0]), d[k][1])
     stalls = {}
     for k, (val, _) in d.items():
         if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
