@@ -43,7 +43,40 @@ typedef struct {
     double seg_max_kernel_us[15]; /* worst time of each kernel segment        */
     int32_t min_blocks;           /* fewest participating blocks in a launch  */
     int32_t max_blocks;           /* most participating blocks in a launch    */
+    double seg_max_span_us[15];   /* worst on-GPU span of each kernel segment:
+                                   * first participating block's start to the
+                                   * last one's end (%globaltimer)            */
+    double max_bus_wait_us;       /* worst wait for the bus (arbiter mode)    */
+    int32_t cpu_mode;             /* CPU mode actually applied (see below)    */
+    int32_t bus_mode;             /* bus mode actually applied                */
+    /* the launch with the worst span of each kernel segment: first -> last
+     * participating block start, fewest / most work items a participating
+     * block ran */
+    double seg_worst_skew_us[15];
+    int32_t seg_worst_items[15][2];
+    double seg_max_wall_us[15];   /* worst host-observed kernel segment: launch
+                                   * to observed completion (the segment's
+                                   * response as the job sees it)            */
+    double seg_worst_mhz[15];     /* SM clock during the worst-span launch     */
+    double min_mhz;               /* lowest SM clock seen in any launch        */
 } rtgpu_exec_result;
+
+/* Host-side resource models of rtgpu_exec_run (rtgpu_exec_configure):
+ *  cpu_mode 0  every task thread on its own core (no CPU interference: the
+ *              analysis' single preemptive CPU is an over-approximation)
+ *  cpu_mode 1  all task threads on one core under SCHED_FIFO, priorities in
+ *              the tasks' order -- the analysis' preemptive fixed-priority
+ *              CPU (falls back to mode 0 without CAP_SYS_NICE)
+ *  bus_mode 0  copies of different tasks may overlap on the copy engines
+ *  bus_mode 1  one non-preemptive fixed-priority bus: a copy waits until the
+ *              bus is free and it is the highest-priority waiter (Lemma 6's
+ *              model; simulator.py grant_bus)
+ * CPU segments consume thread CPU time (CLOCK_THREAD_CPUTIME_ID), so a
+ * preempted segment still executes its full length. */
+#define RTGPU_EXEC_CPU_PARALLEL 0
+#define RTGPU_EXEC_CPU_FP_ONE_CORE 1
+#define RTGPU_EXEC_BUS_FREE 0
+#define RTGPU_EXEC_BUS_FP 1
 
 const char *rtgpu_exec_last_error(void);
 
@@ -64,8 +97,16 @@ int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items,
                                 int idle_us, const uint32_t *bg_mask, float *ms_out,
                                 int32_t *blocks_out, int32_t *sms_out);
 
-/* Time `reps` pinned-host copies of `bytes` (to_device: H2D, else D2H). */
+/* Host wall time (us) of `reps` empty segment launches on `mask`: memset,
+ * launch and polled completion -- the executor's per-kernel overhead. */
+int rtgpu_exec_launch_us(const uint32_t *mask, int reps, float *us_out);
+
+/* Host wall time (ms) of `reps` pinned-host copies of `bytes` (to_device:
+ * H2D, else D2H): enqueue and polled completion, as the run loop does. */
 int rtgpu_exec_copy_ms(int64_t bytes, int to_device, int reps, float *ms_out);
+
+/* Select the host resource models for subsequent rtgpu_exec_run calls. */
+int rtgpu_exec_configure(int cpu_mode, int bus_mode);
 
 /* Run the task set for horizon_us with periodic releases; per-task results. */
 int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,

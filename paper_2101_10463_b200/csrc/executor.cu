@@ -20,10 +20,16 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <pthread.h>
+#include <sched.h>
+#include <time.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <mutex>
+#include <set>
 #include <thread>
 #include <vector>
 
@@ -37,63 +43,143 @@ __device__ __forceinline__ unsigned smid() {
     return r;
 }
 
+/* per-lane control block, cleared by one memset before every launch */
+struct Ctl {
+    unsigned slots[256];          /* per-SM slot counters                       */
+    unsigned long long work;      /* work-item counter                          */
+    unsigned long long inv_start; /* ~(first participating block's start), max  */
+    unsigned long long end;       /* last participating block's end, max        */
+    unsigned long long last_start;/* last participating block's start           */
+    unsigned trace_n;             /* participating blocks traced                */
+    unsigned pad;
+    unsigned bitems[16];          /* items of the first 16 participating blocks */
+    unsigned long long cyc0, ns0; /* block 0 of the participants: SM clock and */
+    unsigned long long cyc1, ns1; /* global time at its start and end           */
+};
+
 struct SegArgs {
     uint32_t mask[RTGPU_EXEC_MASK_WORDS]; /* partition, by value (no H2D per launch) */
-    unsigned *slots;                      /* per-SM slot counters, zeroed per launch */
-    unsigned long long *work;             /* work counter, zeroed per launch */
+    Ctl *ctl;
     long long items;
     int iters;
     int nslots;
     float *sink;
-    unsigned *trace; /* optional: SM of every participating block (+ count at [0]) */
+    unsigned *trace; /* optional: SM of every participating block */
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+/* work-item claim in the global state space: a generic-address atomic on
+ * sm_100 compiles to ATOM + a shared-window fallback whose branch waits for
+ * the result, putting the round trip on the critical path */
+__device__ __forceinline__ unsigned long long claim(unsigned long long *p) {
+    unsigned long long r;
+    asm volatile("atom.global.add.u64 %0, [%1], 1;"
+                 : "=l"(r)
+                 : "l"(__cvta_generic_to_global(p))
+                 : "memory");
+    return r;
+}
+
+__device__ __forceinline__ void gmax(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.global.max.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned gadd32(unsigned *p, unsigned v) {
+    unsigned r;
+    asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+    return r;
+}
+
+/* Blocks outside the partition read %smid and exit without touching memory:
+ * a launch's other ~6*148 blocks land on every SM, including other tasks'
+ * partitions, and must not steal their issue slots. */
 __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
     __shared__ unsigned slot;
     __shared__ unsigned long long item;
     const unsigned sm = smid();
     if (!((a.mask[sm >> 5] >> (sm & 31)) & 1u)) return;
-    if (threadIdx.x == 0) slot = atomicAdd(&a.slots[sm], 1u);
+    const unsigned long long t_in = gtimer();
+    if (threadIdx.x == 0) slot = gadd32(&a.ctl->slots[sm], 1u);
     __syncthreads();
     if (slot >= (unsigned)a.nslots) return;
-    if (a.trace && threadIdx.x == 0) {
-        unsigned pos = atomicAdd(&a.trace[0], 1u);
-        if (pos < 4095) a.trace[1 + pos] = sm;
+    __shared__ unsigned tpos;
+    if (threadIdx.x == 0) {
+        gmax(&a.ctl->inv_start, ~t_in);
+        gmax(&a.ctl->last_start, t_in);
+        tpos = gadd32(&a.ctl->trace_n, 1u);
+        if (a.trace && tpos < 4096) a.trace[tpos] = sm;
+        if (tpos == 0) {
+            a.ctl->cyc0 = clock64();
+            a.ctl->ns0 = gtimer();
+        }
     }
-    /* synthetic compute work: dependent FMA chains, 4 per thread (ILP).
-     * The next item is claimed before the current one is computed, so the
-     * atomic's round trip (L2-die and contention dependent) overlaps work. */
-    float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f, x3 = x0 + 3.f;
+    /* synthetic compute work: three dependent FMA chains per thread, so one
+     * block (one warp per SM sub-partition) keeps the FMA pipe ~3/4 busy and
+     * the second slot's block fills the rest: interleave ratio
+     * alpha = 2 t2 / t1 ~ 1.5, inside the model's [1, 1.8] (model.py:17).
+     * The next item is claimed before the current one is computed and its
+     * value is only consumed after the FMA loop, so the atomic's round trip
+     * (L2-die and load dependent) never sits on the item's critical path. */
+    float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f;
     __shared__ unsigned long long next;
-    if (threadIdx.x == 0) item = atomicAdd(a.work, 1ull);
+    if (threadIdx.x == 0) item = claim(&a.ctl->work);
     __syncthreads();
     unsigned long long it = item;
+    unsigned done = 0;
     while ((long long)it < a.items) {
-        if (threadIdx.x == 0) next = atomicAdd(a.work, 1ull);
-        for (int k = 0; k < a.iters; k++) {
+        done++;
+        unsigned long long nx = 0;
+        if (threadIdx.x == 0) nx = claim(&a.ctl->work); /* in flight during the loop */
+        const int iters = a.iters;
+#pragma unroll 4
+        for (int k = 0; k < iters; k++) {
             x0 = fmaf(x0, 0.9999999f, 0.5f);
             x1 = fmaf(x1, 0.9999999f, 0.5f);
             x2 = fmaf(x2, 0.9999999f, 0.5f);
-            x3 = fmaf(x3, 0.9999999f, 0.5f);
         }
+        if (threadIdx.x == 0) next = nx;
         __syncthreads();
         it = next;
         __syncthreads();
     }
-    if (x0 + x1 + x2 + x3 == 12345.f) a.sink[blockIdx.x] = x0;
+    if (threadIdx.x == 0) {
+        gmax(&a.ctl->end, gtimer());
+        if (tpos < 16) a.ctl->bitems[tpos] = done;
+        if (tpos == 0) {
+            a.ctl->cyc1 = clock64();
+            a.ctl->ns1 = gtimer();
+        }
+    }
+    if (x0 + x1 + x2 == 12345.f) a.sink[blockIdx.x] = x0;
 }
 
 char g_err[256] = "";
 
+constexpr int RING = 16; /* control blocks / event pairs per lane: one per kernel of a job */
+
 struct Lane {
     cudaStream_t st = nullptr;
-    unsigned *slots = nullptr;
-    unsigned long long *work = nullptr;
+    Ctl *ring = nullptr;  /* device control blocks, one per kernel segment of a job */
+    Ctl *hring = nullptr; /* pinned host copies, read back after the job */
+    Ctl *ctl = nullptr;   /* the control block of the next launch */
+    Ctl *hctl = nullptr;
     float *sink = nullptr;
     unsigned *trace = nullptr;
     void *hbuf = nullptr, *dbuf = nullptr;
     size_t buf = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t k0[RING] = {}, k1[RING] = {};
+    cudaEvent_t ev_wait = nullptr; /* blocking-sync: a waiting thread sleeps */
+    bool spin = false;             /* waits poll instead of sleeping (own core) */
+    void use(int k) {
+        ctl = ring + k;
+        hctl = hring + k;
+    }
 };
 
 int sm_count() {
@@ -105,8 +191,9 @@ int sm_count() {
 
 int lane_init(Lane &L, size_t buf) {
     if (cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking) != cudaSuccess) return -1;
-    if (cudaMalloc(&L.slots, 256 * sizeof(unsigned)) != cudaSuccess) return -1;
-    if (cudaMalloc(&L.work, sizeof(unsigned long long)) != cudaSuccess) return -1;
+    if (cudaMalloc(&L.ring, RING * sizeof(Ctl)) != cudaSuccess) return -1;
+    if (cudaMallocHost(&L.hring, RING * sizeof(Ctl)) != cudaSuccess) return -1;
+    L.use(0);
     if (cudaMalloc(&L.sink, 8192 * sizeof(float)) != cudaSuccess) return -1;
     if (cudaMalloc(&L.trace, 4096 * sizeof(unsigned)) != cudaSuccess) return -1;
     L.buf = buf < 64 ? 64 : buf;
@@ -115,19 +202,41 @@ int lane_init(Lane &L, size_t buf) {
     memset(L.hbuf, 1, L.buf);
     cudaEventCreate(&L.e0);
     cudaEventCreate(&L.e1);
+    for (int k = 0; k < RING; k++) {
+        cudaEventCreate(&L.k0[k]);
+        cudaEventCreate(&L.k1[k]);
+    }
+    cudaEventCreateWithFlags(&L.ev_wait, cudaEventBlockingSync | cudaEventDisableTiming);
     return 0;
 }
 
 void lane_free(Lane &L) {
     if (L.st) cudaStreamDestroy(L.st);
-    cudaFree(L.slots);
-    cudaFree(L.work);
+    cudaFree(L.ring);
+    cudaFreeHost(L.hring);
     cudaFree(L.sink);
     cudaFree(L.trace);
     cudaFreeHost(L.hbuf);
     cudaFree(L.dbuf);
     if (L.e0) cudaEventDestroy(L.e0);
     if (L.e1) cudaEventDestroy(L.e1);
+    for (int k = 0; k < RING; k++) {
+        if (L.k0[k]) cudaEventDestroy(L.k0[k]);
+        if (L.k1[k]) cudaEventDestroy(L.k1[k]);
+    }
+    if (L.ev_wait) cudaEventDestroy(L.ev_wait);
+}
+
+/* wait for the lane's stream: poll when the thread owns its core (no
+ * wake-up latency), else sleep so lower-priority threads on the core run */
+void lane_wait(Lane &L) {
+    cudaEventRecord(L.ev_wait, L.st);
+    if (L.spin) {
+        while (cudaEventQuery(L.ev_wait) == cudaErrorNotReady) {
+        }
+    } else {
+        cudaEventSynchronize(L.ev_wait);
+    }
 }
 
 /* enqueue one GPU segment on the lane's stream */
@@ -135,18 +244,48 @@ void enqueue_segment(Lane &L, const uint32_t *mask, int nslots, long long items,
                      bool trace) {
     SegArgs a;
     memcpy(a.mask, mask, sizeof a.mask);
-    a.slots = L.slots;
-    a.work = L.work;
+    a.ctl = L.ctl;
     a.items = items;
     a.iters = iters;
     a.nslots = nslots;
     a.sink = L.sink;
     a.trace = trace ? L.trace : nullptr;
-    cudaMemsetAsync(L.slots, 0, 256 * sizeof(unsigned), L.st);
-    cudaMemsetAsync(L.work, 0, sizeof(unsigned long long), L.st);
-    if (trace) cudaMemsetAsync(L.trace, 0, sizeof(unsigned), L.st);
+    cudaMemsetAsync(L.ctl, 0, sizeof(Ctl), L.st);
     const int grid = sm_count() * RTGPU_EXEC_BLOCKS_PER_SM;
     persistent_segment<<<grid, 128, 0, L.st>>>(a);
+}
+
+/* the last launch's participating blocks and on-GPU span (us); enqueues a
+ * D2H of the control block and waits */
+struct LaunchDetail {
+    double skew_us;     /* first -> last participating block start             */
+    int items_min, items_max;
+    double mhz;         /* SM clock over the first participant's run            */
+};
+
+void decode_ctl(const Ctl &c, unsigned *nb, double *span_us, LaunchDetail *d);
+
+void lane_readback(Lane &L, unsigned *nb, double *span_us, LaunchDetail *d = nullptr) {
+    cudaMemcpyAsync(L.hctl, L.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, L.st);
+    lane_wait(L);
+    decode_ctl(*L.hctl, nb, span_us, d);
+}
+
+void decode_ctl(const Ctl &c, unsigned *nb, double *span_us, LaunchDetail *d) {
+    *nb = c.trace_n;
+    const unsigned long long t0 = ~c.inv_start, t1 = c.end;
+    *span_us = (c.inv_start && t1 >= t0) ? (double)(t1 - t0) * 1e-3 : 0.0;
+    if (d) {
+        d->skew_us = (c.inv_start && c.last_start >= t0) ? (double)(c.last_start - t0) * 1e-3 : 0.0;
+        d->mhz = (c.ns1 > c.ns0 && c.cyc1 > c.cyc0) ? (double)(c.cyc1 - c.cyc0) * 1e3 / (double)(c.ns1 - c.ns0)
+                                                   : 0.0;
+        d->items_min = 1 << 30;
+        d->items_max = 0;
+        for (unsigned b = 0; b < std::min(c.trace_n, 16u); b++) {
+            d->items_min = std::min(d->items_min, (int)c.bitems[b]);
+            d->items_max = std::max(d->items_max, (int)c.bitems[b]);
+        }
+    }
 }
 
 typedef std::chrono::steady_clock clk;
@@ -155,10 +294,69 @@ inline double us_since(clk::time_point t0) {
     return std::chrono::duration<double, std::micro>(clk::now() - t0).count();
 }
 
+double thread_cpu_us() {
+    timespec ts;
+    clock_gettime(CLOCK_THREAD_CPUTIME_ID, &ts);
+    return (double)ts.tv_sec * 1e6 + (double)ts.tv_nsec * 1e-3;
+}
+
+/* execute `us` of CPU work: spin until the thread has consumed that much CPU
+ * time (a preempted segment resumes where it stopped, as in the model) */
 void spin_us(double us) {
-    auto t0 = clk::now();
-    while (us_since(t0) < us) {
+    const double t0 = thread_cpu_us();
+    while (thread_cpu_us() - t0 < us) {
     }
+}
+
+/* One non-preemptive fixed-priority bus (simulator.py grant_bus): a copy
+ * starts when the bus is free and no higher-priority copy is waiting. */
+struct Bus {
+    std::mutex mu;
+    std::condition_variable cv;
+    bool busy = false;
+    std::multiset<int> waiting; /* priorities: lower value = higher priority */
+    void acquire(int prio, bool poll) {
+        std::unique_lock<std::mutex> lk(mu);
+        auto it = waiting.insert(prio);
+        if (poll) { /* the thread owns its core: no wake-up latency */
+            while (busy || *waiting.begin() != prio) {
+                lk.unlock();
+                lk.lock();
+            }
+        } else {
+            cv.wait(lk, [&] { return !busy && *waiting.begin() == prio; });
+        }
+        waiting.erase(it);
+        busy = true;
+    }
+    void release() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            busy = false;
+        }
+        cv.notify_all();
+    }
+};
+
+int g_cpu_mode = RTGPU_EXEC_CPU_PARALLEL;
+int g_bus_mode = RTGPU_EXEC_BUS_FP;
+
+/* the CPUs this process may run on, highest first */
+std::vector<int> allowed_cpus() {
+    std::vector<int> out;
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    if (sched_getaffinity(0, sizeof set, &set) == 0)
+        for (int c = CPU_SETSIZE - 1; c >= 0; c--)
+            if (CPU_ISSET(c, &set)) out.push_back(c);
+    return out;
+}
+
+bool pin_thread(int cpu) {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    CPU_SET(cpu, &set);
+    return pthread_setaffinity_np(pthread_self(), sizeof set, &set) == 0;
 }
 
 }  // namespace
@@ -210,13 +408,16 @@ int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items,
         cudaEventElapsedTime(&ms_out[r], L.e0, L.e1);
         if (r == 0 && (blocks_out || sms_out)) {
             std::vector<unsigned> tr(4096);
+            unsigned nb = 0;
+            double span = 0;
+            lane_readback(L, &nb, &span);
+            nb = std::min(nb, 4096u);
             cudaMemcpy(tr.data(), L.trace, 4096 * sizeof(unsigned), cudaMemcpyDeviceToHost);
-            unsigned nb = std::min(tr[0], 4095u);
             std::vector<int> per(256, 0);
             int distinct = 0;
             bool outside = false;
             for (unsigned b = 0; b < nb; b++) {
-                unsigned s = tr[1 + b];
+                unsigned s = tr[b];
                 if (s >= 256 || !((mask[s >> 5] >> (s & 31)) & 1u)) outside = true;
                 else if (per[s]++ == 0) distinct++;
             }
@@ -226,7 +427,7 @@ int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items,
     }
     if (loaded) {
         const unsigned long long stop = (unsigned long long)1 << 41;
-        cudaMemcpy(B.work, &stop, sizeof stop, cudaMemcpyHostToDevice);
+        cudaMemcpy(&B.ctl->work, &stop, sizeof stop, cudaMemcpyHostToDevice);
         cudaStreamSynchronize(B.st);
         lane_free(B);
     }
@@ -245,26 +446,115 @@ int rtgpu_exec_copy_ms(int64_t bytes, int to_device, int reps, float *ms_out) {
         strcpy(g_err, "executor allocation failed");
         return -1;
     }
+    L.spin = true;
     for (int r = -1; r < reps; r++) {
-        cudaEventRecord(L.e0, L.st);
+        /* host wall time of the run loop's copy path: enqueue + polled completion */
+        const auto t0 = clk::now();
         if (to_device) cudaMemcpyAsync(L.dbuf, L.hbuf, bytes, cudaMemcpyHostToDevice, L.st);
         else cudaMemcpyAsync(L.hbuf, L.dbuf, bytes, cudaMemcpyDeviceToHost, L.st);
-        cudaEventRecord(L.e1, L.st);
-        cudaEventSynchronize(L.e1);
-        if (r >= 0) cudaEventElapsedTime(&ms_out[r], L.e0, L.e1);
+        lane_wait(L);
+        if (r >= 0) ms_out[r] = (float)(us_since(t0) * 1e-3);
     }
     lane_free(L);
     return 0;
 }
 
+int rtgpu_exec_launch_us(const uint32_t *mask, int reps, float *us_out) {
+    Lane L;
+    if (lane_init(L, 64)) {
+        strcpy(g_err, "executor allocation failed");
+        return -1;
+    }
+    L.spin = true;
+    for (int r = -1; r < reps; r++) {
+        /* the run loop's kernel path with no work: memset, launch, polled completion */
+        const auto t0 = clk::now();
+        enqueue_segment(L, mask, 2, 0, 1, false);
+        lane_wait(L);
+        if (r >= 0) us_out[r] = (float)us_since(t0);
+    }
+    cudaError_t e = cudaGetLastError();
+    lane_free(L);
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof g_err, "launch: %s", cudaGetErrorString(e));
+        return -2;
+    }
+    return 0;
+}
+
+/* Interference probe: `reps` launches of a segment on `mask` (nslots, items,
+ * iters) while a background host thread keeps one load running until done:
+ * load 0 none, 1 back-to-back H2D+D2H copies of `bytes`, 2 back-to-back
+ * launches of an empty segment whose blocks all exit (other partitions'
+ * grids), 3 a long segment on bg_mask.  Outputs each launch's on-GPU span. */
+int rtgpu_exec_probe(const uint32_t *mask, int nslots, int64_t items, int iters, int reps, int load,
+                     int64_t bytes, const uint32_t *bg_mask, float *span_us_out) {
+    Lane L, B;
+    if (lane_init(L, 64) || lane_init(B, (size_t)std::max<int64_t>(bytes, 64))) {
+        strcpy(g_err, "executor allocation failed");
+        return -1;
+    }
+    L.spin = B.spin = true;
+    std::atomic<bool> stop{false};
+    uint32_t none[RTGPU_EXEC_MASK_WORDS] = {0};
+    std::thread bg([&]() {
+        if (load == 3) enqueue_segment(B, bg_mask, 2, (long long)1 << 40, iters, false);
+        while (!stop.load()) {
+            if (load == 1) {
+                cudaMemcpyAsync(B.dbuf, B.hbuf, (size_t)bytes, cudaMemcpyHostToDevice, B.st);
+                cudaMemcpyAsync(B.hbuf, B.dbuf, (size_t)bytes, cudaMemcpyDeviceToHost, B.st);
+                lane_wait(B);
+            } else if (load == 2) {
+                enqueue_segment(B, none, 2, 0, 1, false);
+                lane_wait(B);
+            } else {
+                std::this_thread::sleep_for(std::chrono::microseconds(200));
+            }
+        }
+    });
+    std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    for (int r = 0; r < reps; r++) {
+        enqueue_segment(L, mask, nslots, items, iters, false);
+        unsigned nb;
+        double span;
+        lane_readback(L, &nb, &span);
+        span_us_out[r] = (float)span;
+    }
+    stop = true;
+    bg.join();
+    if (load == 3) {
+        const unsigned long long stopw = (unsigned long long)1 << 41;
+        cudaMemcpy(&B.ctl->work, &stopw, sizeof stopw, cudaMemcpyHostToDevice);
+    }
+    cudaDeviceSynchronize();
+    cudaError_t e = cudaGetLastError();
+    lane_free(L);
+    lane_free(B);
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof g_err, "probe: %s", cudaGetErrorString(e));
+        return -2;
+    }
+    return 0;
+}
+
+int rtgpu_exec_configure(int cpu_mode, int bus_mode) {
+    if (cpu_mode < 0 || cpu_mode > 1 || bus_mode < 0 || bus_mode > 1) {
+        strcpy(g_err, "rtgpu_exec_configure: unknown mode");
+        return -1;
+    }
+    g_cpu_mode = cpu_mode;
+    g_bus_mode = bus_mode;
+    return 0;
+}
+
 /*
  * Run the task set for `horizon_us`: each task is a host thread releasing
- * jobs every period; a job runs its segments in order (CPU: busy wait on the
- * host; copy: cudaMemcpyAsync on the task's stream; kernel: persistent
- * segment pinned to the task's SM partition) and its response time is
- * release -> end of the last CPU segment.  Jobs of one task run in order;
- * a release while the previous job still runs waits for it (the sporadic
- * task model's constrained deadlines make this rare).
+ * jobs every period; a job runs its segments in order (CPU: thread CPU time
+ * on the host; copy: cudaMemcpyAsync on the task's stream, through the bus
+ * arbiter in bus mode 1; kernel: persistent segment pinned to the task's SM
+ * partition) and its response time is release -> end of the last CPU
+ * segment.  Jobs of one task run in order; a release while the previous job
+ * still runs waits for it (constrained deadlines make this rare).
  */
 int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
                    rtgpu_exec_result *results) {
@@ -282,7 +572,16 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
         }
         memset(&results[i], 0, sizeof(rtgpu_exec_result));
     }
-    std::atomic<int> ready{0};
+    /* priority rank of every task (0 = highest) */
+    std::vector<int> rank(n_tasks, 0);
+    for (int i = 0; i < n_tasks; i++)
+        for (int j = 0; j < n_tasks; j++)
+            if (tasks[j].priority < tasks[i].priority || (tasks[j].priority == tasks[i].priority && j < i))
+                rank[i]++;
+    const std::vector<int> cpus = allowed_cpus();
+    const int cpu_mode = g_cpu_mode, bus_mode = g_bus_mode;
+    std::atomic<int> fifo_fail{0};
+    Bus bus;
     auto t_start = clk::now() + std::chrono::milliseconds(50);
     std::vector<std::thread> th;
     for (int i = 0; i < n_tasks; i++) {
@@ -290,66 +589,118 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
             const rtgpu_exec_task &t = tasks[i];
             Lane &L = lanes[i];
             rtgpu_exec_result &R = results[i];
-            ready++;
-            std::this_thread::sleep_until(t_start);
+            bool own_core = true;
+            if (!cpus.empty()) {
+                if (cpu_mode == RTGPU_EXEC_CPU_FP_ONE_CORE) {
+                    pin_thread(cpus[0]);
+                    sched_param sp;
+                    sp.sched_priority = 80 - rank[i];
+                    if (pthread_setschedparam(pthread_self(), SCHED_FIFO, &sp) == 0) {
+                        own_core = false;
+                    } else {
+                        fifo_fail++; /* no FP CPU: do not time-share one core */
+                        pin_thread(cpus[(size_t)rank[i] % cpus.size()]);
+                    }
+                } else {
+                    pin_thread(cpus[(size_t)rank[i] % cpus.size()]);
+                }
+            }
+            /* a thread that owns its core polls every wait (bus, stream,
+             * release): no wake-up latency enters the response times */
+            L.spin = own_core;
             double sum = 0;
+            auto copy = [&](int idx, bool h2d) {
+                const auto w0 = clk::now();
+                if (bus_mode == RTGPU_EXEC_BUS_FP) bus.acquire(t.priority, own_core);
+                R.max_bus_wait_us = std::max(R.max_bus_wait_us, us_since(w0));
+                const auto c0 = clk::now();
+                if (h2d)
+                    cudaMemcpyAsync(L.dbuf, L.hbuf, (size_t)t.copy_bytes[idx], cudaMemcpyHostToDevice, L.st);
+                else
+                    cudaMemcpyAsync(L.hbuf, L.dbuf, (size_t)t.copy_bytes[idx], cudaMemcpyDeviceToHost, L.st);
+                lane_wait(L);
+                if (bus_mode == RTGPU_EXEC_BUS_FP) bus.release();
+                R.max_copy_us = std::max(R.max_copy_us, us_since(c0));
+            };
             for (int64_t k = 0;; k++) {
                 double release = (double)k * t.period_us;
                 if (release >= horizon_us) break;
                 auto rel_tp = t_start + std::chrono::microseconds((int64_t)release);
-                std::this_thread::sleep_until(rel_tp);
-                int copy = 0;
+                if (own_core) {
+                    std::this_thread::sleep_until(rel_tp - std::chrono::microseconds(500));
+                    while (clk::now() < rel_tp) {
+                    }
+                } else {
+                    std::this_thread::sleep_until(rel_tp);
+                }
+                int cp = 0;
+                double wall[RING] = {0};
                 for (int s = 0; s < t.m; s++) {
                     spin_us((double)t.cpu_us[s]);
                     if (s == t.m - 1) break;
                     /* memory copies and the kernel between CPU segments s and s+1 */
-                    auto seg_t0 = clk::now();
-                    if (copy < t.n_copies) {
-                        cudaMemcpyAsync(L.dbuf, L.hbuf, (size_t)t.copy_bytes[copy++],
-                                        cudaMemcpyHostToDevice, L.st);
-                        cudaStreamSynchronize(L.st);
-                    }
-                    double c0 = us_since(seg_t0);
-                    R.max_copy_us = std::max(R.max_copy_us, c0);
+                    if (cp < t.n_copies) copy(cp++, true);
                     auto k0 = clk::now();
-                    cudaMemsetAsync(L.trace, 0, sizeof(unsigned), L.st);
-                    cudaEventRecord(L.e0, L.st);
+                    L.use(s);
+                    cudaEventRecord(L.k0[s], L.st);
                     enqueue_segment(L, t.sm_mask, t.slots_per_sm, t.kernel_items[s], t.kernel_iters,
                                     true);
-                    cudaEventRecord(L.e1, L.st);
-                    unsigned nb = 0;
-                    cudaMemcpyAsync(&nb, L.trace, sizeof(unsigned), cudaMemcpyDeviceToHost, L.st);
-                    cudaStreamSynchronize(L.st);
-                    float kms = 0;
-                    cudaEventElapsedTime(&kms, L.e0, L.e1);
-                    R.max_kernel_us = std::max(R.max_kernel_us, (double)kms * 1e3);
-                    R.seg_max_kernel_us[s] = std::max(R.seg_max_kernel_us[s], (double)kms * 1e3);
-                    if (R.min_blocks == 0 || (int)nb < R.min_blocks) R.min_blocks = (int)nb;
-                    R.max_blocks = std::max(R.max_blocks, (int)nb);
-                    R.max_kernel_wall_us = std::max(R.max_kernel_wall_us, us_since(k0));
-                    if (t.two_copy && copy < t.n_copies) {
-                        auto d0 = clk::now();
-                        cudaMemcpyAsync(L.hbuf, L.dbuf, (size_t)t.copy_bytes[copy++],
-                                        cudaMemcpyDeviceToHost, L.st);
-                        cudaStreamSynchronize(L.st);
-                        R.max_copy_us = std::max(R.max_copy_us, us_since(d0));
-                    }
+                    cudaEventRecord(L.k1[s], L.st);
+                    lane_wait(L);
+                    wall[s] = us_since(k0);
+                    if (t.two_copy && cp < t.n_copies) copy(cp++, false);
                 }
                 double resp = std::chrono::duration<double, std::micro>(clk::now() - rel_tp).count();
                 R.jobs++;
                 sum += resp;
                 R.max_response_us = std::max(R.max_response_us, resp);
                 if (resp > (double)t.deadline_us) R.deadline_misses++;
+                /* the job's kernel records, read back off its critical path */
+                const int nk = t.m - 1;
+                if (nk > 0) {
+                    cudaMemcpyAsync(L.hring, L.ring, nk * sizeof(Ctl), cudaMemcpyDeviceToHost, L.st);
+                    lane_wait(L);
+                }
+                for (int s = 0; s < nk; s++) {
+                    unsigned nb = 0;
+                    double span = 0;
+                    LaunchDetail det;
+                    decode_ctl(L.hring[s], &nb, &span, &det);
+                    if (span > R.seg_max_span_us[s]) {
+                        R.seg_worst_skew_us[s] = det.skew_us;
+                        R.seg_worst_items[s][0] = det.items_min;
+                        R.seg_worst_items[s][1] = det.items_max;
+                        R.seg_worst_mhz[s] = det.mhz;
+                    }
+                    if (det.mhz > 0 && (R.min_mhz == 0 || det.mhz < R.min_mhz)) R.min_mhz = det.mhz;
+                    float kms = 0;
+                    cudaEventElapsedTime(&kms, L.k0[s], L.k1[s]);
+                    R.max_kernel_us = std::max(R.max_kernel_us, (double)kms * 1e3);
+                    R.seg_max_kernel_us[s] = std::max(R.seg_max_kernel_us[s], (double)kms * 1e3);
+                    R.seg_max_wall_us[s] = std::max(R.seg_max_wall_us[s], wall[s]);
+                    R.seg_max_span_us[s] = std::max(R.seg_max_span_us[s], span);
+                    if (R.min_blocks == 0 || (int)nb < R.min_blocks) R.min_blocks = (int)nb;
+                    R.max_blocks = std::max(R.max_blocks, (int)nb);
+                    R.max_kernel_wall_us = std::max(R.max_kernel_wall_us, wall[s]);
+                }
             }
             R.mean_response_us = R.jobs ? sum / (double)R.jobs : 0;
         });
     }
     for (auto &x : th) x.join();
+    for (int i = 0; i < n_tasks; i++) {
+        results[i].cpu_mode = (cpu_mode == RTGPU_EXEC_CPU_FP_ONE_CORE && fifo_fail == 0)
+                                  ? RTGPU_EXEC_CPU_FP_ONE_CORE : RTGPU_EXEC_CPU_PARALLEL;
+        results[i].bus_mode = bus_mode;
+    }
     cudaError_t e = cudaGetLastError();
     for (auto &L : lanes) lane_free(L);
     if (e != cudaSuccess) {
         snprintf(g_err, sizeof g_err, "run: %s", cudaGetErrorString(e));
         return -2;
+    }
+    if (cpu_mode == RTGPU_EXEC_CPU_FP_ONE_CORE && fifo_fail > 0) {
+        snprintf(g_err, sizeof g_err, "SCHED_FIFO unavailable: ran with a core per task");
     }
     return 0;
 }

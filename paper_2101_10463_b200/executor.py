@@ -45,7 +45,16 @@ class ExecResultC(ctypes.Structure):
                 ("max_response_us", ctypes.c_double), ("mean_response_us", ctypes.c_double),
                 ("max_kernel_us", ctypes.c_double), ("max_kernel_wall_us", ctypes.c_double),
                 ("max_copy_us", ctypes.c_double), ("seg_max_kernel_us", ctypes.c_double * 15),
-                ("min_blocks", ctypes.c_int32), ("max_blocks", ctypes.c_int32)]
+                ("min_blocks", ctypes.c_int32), ("max_blocks", ctypes.c_int32),
+                ("seg_max_span_us", ctypes.c_double * 15), ("max_bus_wait_us", ctypes.c_double),
+                ("cpu_mode", ctypes.c_int32), ("bus_mode", ctypes.c_int32),
+                ("seg_worst_skew_us", ctypes.c_double * 15),
+                ("seg_worst_items", (ctypes.c_int32 * 2) * 15),
+                ("seg_max_wall_us", ctypes.c_double * 15),
+                ("seg_worst_mhz", ctypes.c_double * 15), ("min_mhz", ctypes.c_double)]
+
+CPU_PARALLEL, CPU_FP_ONE_CORE = 0, 1   # include/rtgpu_exec.h host resource models
+BUS_FREE, BUS_FP = 0, 1
 
 
 def _lib():
@@ -71,6 +80,9 @@ def _lib():
                                          ctypes.POINTER(ctypes.c_float)]
         L.rtgpu_exec_run.argtypes = [ctypes.POINTER(ExecTaskC), ctypes.c_int, ctypes.c_double,
                                      ctypes.POINTER(ExecResultC)]
+        L.rtgpu_exec_launch_us.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_float)]
+        L.rtgpu_exec_configure.argtypes = [ctypes.c_int, ctypes.c_int]
         L.rtgpu_exec_last_error.restype = ctypes.c_char_p
         L._exec_ready = True
     return L
@@ -110,6 +122,16 @@ def kernel_ms(sms, nslots: int, items: int, iters: int, reps: int = 5, idle_us: 
     return [float(x) for x in out], nb.value, ns.value
 
 
+def launch_us(sms, reps: int = 20):
+    """Host wall time (us) of empty segment launches: the per-kernel overhead
+    the job path pays (memset, launch, polled completion)."""
+    _native.require_device()
+    out = (ctypes.c_float * reps)()
+    if _lib().rtgpu_exec_launch_us(mask_of(sms), reps, out):
+        raise RuntimeError(_lib().rtgpu_exec_last_error().decode())
+    return [float(x) for x in out]
+
+
 def copy_ms(nbytes: int, to_device: bool, reps: int = 5):
     out = (ctypes.c_float * reps)()
     if _lib().rtgpu_exec_copy_ms(nbytes, 1 if to_device else 0, reps, out):
@@ -147,6 +169,9 @@ class WcrtReport:
     max_ratio: float = 0.0
     max_kernel_ratio: float = 0.0  # worst measured kernel time / its Lemma-4 bound
     horizon_us: float = 0.0
+    cpu_mode: int = CPU_PARALLEL
+    bus_mode: int = BUS_FP
+    calibration: list = field(default_factory=list)  # per kernel: items, t1, t2, alpha
     note: str = ""
 
 
@@ -170,13 +195,19 @@ def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = 0.12
         t1 += kernel_ms_loaded([sm], others, 1, items, iters, 2)[0]
         t2 += kernel_ms_loaded([sm], others, 2, items, iters, 2)[0]
     t1u, t2u = max(t1) * 1e3, max(t2) * 1e3
-    alpha = Fraction(max(100, min(180, math.ceil(200 * t2u / t1u))), 100)
+    pct = math.ceil(200 * t2u / t1u)
+    if pct > 180:  # MAX_INTERLEAVE_RATIO (model.py:17): the model cannot bound this kernel
+        raise ValueError(f"measured interleave ratio {pct / 100} exceeds the model's 1.8")
+    alpha = Fraction(max(100, pct), 100)
     return KernelCal(items, iters, t1u, t2u, alpha, int(min(t1) * 1e3 * 0.95),
                      _ceil_margin(t1u, margin))
 
 
-def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = True):
+def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = True,
+              cpu_mode: int = CPU_PARALLEL, bus_mode: int = BUS_FP):
     L = _lib()
+    if L.rtgpu_exec_configure(cpu_mode, bus_mode):
+        raise ValueError(L.rtgpu_exec_last_error().decode())
     n = len(defs)
     arr = (ExecTaskC * n)()
     for i, (d, sms) in enumerate(zip(defs, partitions)):
@@ -206,7 +237,8 @@ def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = 
 
 def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int = 0,
                     utilization: float = 3.0, horizon_us: float = 3e6, n_sm: int = 148,
-                    margin: float = 0.12) -> WcrtReport:
+                    margin: float = 0.12, cpu_mode: int = CPU_PARALLEL,
+                    bus_mode: int = BUS_FP) -> WcrtReport:
     """BASELINE config 4: n concurrent tasks on disjoint SM partitions of the
     GPU; measured WCRT vs the RTGPU bound R_k."""
     _native.require_device()
@@ -223,8 +255,10 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
         for it in d.kernel_items:
             if it not in cal:
                 cal[it] = calibrate_kernel(it, iters, margin=margin)
-    overhead = max(kernel_ms(list(range(8)), 2, 0, iters, 5)[0] +
-                   kernel_ms(list(range(8)), 2, 0, iters, 3, 20000)[0]) * 1e3
+    # critical-path overhead GL: host wall time of an empty launch (what the
+    # job path adds around every kernel), worst of many
+    overhead = max(launch_us(list(range(8)), 50) +
+                   [x * 1e3 for x in kernel_ms(list(range(8)), 2, 0, iters, 3, 20000)[0]])
     GL = _ceil_margin(overhead, margin)
     copy_cal = {}
     for d in defs:
@@ -256,6 +290,9 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
     ts = TaskSet(tuple(specs), MemModel.TWO_COPY, PlatformConfig(n_sm, Fraction(3, 25)))
     report = analyze_rtgpu(ts)
     out = WcrtReport(schedulable=report.schedulable, horizon_us=horizon_us)
+    out.calibration = [{"items": c.items, "t1_us": round(c.t1_us, 1), "t2_us": round(c.t2_us, 1),
+                        "alpha": str(c.alpha), "gw_hi_us": c.hi_us, "gl_us": GL}
+                       for c in cal.values()]
     if not report.schedulable:
         out.note = "analysis rejects the calibrated task set; nothing to execute"
         return out
@@ -267,14 +304,16 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
         parts.append(list(range(nxt, nxt + gn)))
         nxt += gn
     out.allocation = {s.id: alloc[s.id] for s in specs}
-    res = run_tasks(defs, parts, iters, horizon_us)
+    res = run_tasks(defs, parts, iters, horizon_us, cpu_mode=cpu_mode, bus_mode=bus_mode)
+    out.cpu_mode, out.bus_mode = int(res[0].cpu_mode), int(res[0].bus_mode)
     ratios, kok = [], True
     for s, d, r, sms in zip(specs, defs, res, parts):
         bound = report.per_task[s.id].end_to_end_up
         grs = [gpu_response_bounds(g, 2 * len(sms)).hi for g in s.gpu_segments]
         ratio = r.max_response_us / float(bound)
         ratios.append(ratio)
-        seg = [r.seg_max_kernel_us[j] for j in range(len(grs))]
+        # the segment's response as the job sees it: launch to observed completion
+        seg = [r.seg_max_wall_us[j] for j in range(len(grs))]
         kern_ok = all(x <= float(b) for x, b in zip(seg, grs))
         kok = kok and kern_ok
         out.max_kernel_ratio = max([out.max_kernel_ratio] + [x / float(b) for x, b in zip(seg, grs)])
@@ -285,6 +324,18 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
                           "max_kernel_us": round(r.max_kernel_us, 1),
                           "kernel_us_vs_gr_up": [[round(x, 1), round(float(b), 1)]
                                                  for x, b in zip(seg, grs)],
+                          "kernel_span_us": [round(r.seg_max_span_us[j], 1)
+                                             for j in range(len(grs))],
+                          "kernel_event_us": [round(r.seg_max_kernel_us[j], 1)
+                                              for j in range(len(grs))],
+                          "worst_launch": [{"skew_us": round(r.seg_worst_skew_us[j], 1),
+                                            "sm_mhz": round(r.seg_worst_mhz[j]),
+                                            "items": [int(r.seg_worst_items[j][0]),
+                                                      int(r.seg_worst_items[j][1])]}
+                                           for j in range(len(grs))],
+                          "min_sm_mhz": round(r.min_mhz),
+                          "max_copy_us": round(r.max_copy_us, 1),
+                          "max_bus_wait_us": round(r.max_bus_wait_us, 1),
                           "blocks_per_launch": [int(r.min_blocks), int(r.max_blocks)],
                           "gr_up_us": float(max(grs)), "deadline_us": d.deadline_us,
                           "deadline_misses": int(r.deadline_misses)})
