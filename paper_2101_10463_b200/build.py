@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librtgpu.so")
 SOURCES = ["rtgpu_engine.cu", "rtgpu_k_f64.cu", "rtgpu_k_i64.cu", "rtgpu_k_i128.cu",
-           "taskgen.cpp", "executor.cu"]
+           "taskgen.cpp", "executor.cu", "simulator.cu"]
 HEADERS = ["engine_core.cuh", "kernel.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -27,7 +27,7 @@ OBJDIR = os.path.join(HERE, "build")
 
 def _inputs():
     out = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
-    out += [os.path.join(ROOT, "include", h) for h in ("rtgpu.h", "rtgpu_gen.h", "rtgpu_exec.h")]
+    out += [os.path.join(ROOT, "include", h) for h in ("rtgpu.h", "rtgpu_gen.h", "rtgpu_exec.h", "rtgpu_sim.h")]
     return out
 
 
