@@ -34,7 +34,10 @@ extern "C" {
  *   [6] S_max (longest job segment plan)
  *   [7] word offset of the key from the blob start: L words, the 32-bit
  *       init_by_array key random.Random(seed) derives from the seed
- *   [8..15] reserved
+ *   [8] job-record pool size P (0 = R): records of finished jobs past
+ *       their deadline are recycled; a run needing more than P live jobs
+ *       stops with RTGPU_SIM_POOL_OVERFLOW (re-run it with P = R)
+ *   [9..15] reserved
  * task records (RTGPU_SIM_TASK words, priority order, highest first):
  *   [0] S plan length  [1] period  [2] deadline  [3] priority
  *   [4] word offset of the task's plan entries from the blob start
@@ -58,7 +61,8 @@ enum { RTGPU_EV_RELEASE = 0, RTGPU_EV_START, RTGPU_EV_PREEMPT, RTGPU_EV_RESUME, 
 enum { RTGPU_KIND_CPU = 0, RTGPU_KIND_MEM, RTGPU_KIND_GPU, RTGPU_KIND_JOB };
 
 /* per-simulation status */
-enum { RTGPU_SIM_OK = 0, RTGPU_SIM_BAD_INPUT = 1, RTGPU_SIM_EVENT_OVERFLOW = 2 };
+enum { RTGPU_SIM_OK = 0, RTGPU_SIM_BAD_INPUT = 1, RTGPU_SIM_EVENT_OVERFLOW = 2,
+       RTGPU_SIM_POOL_OVERFLOW = 3 };
 
 /* One event: time (scaled) and packed fields
  *   bits 0..31 job index, 32..39 task (priority order), 40..43 kind,
@@ -103,11 +107,13 @@ int rtgpu_sim_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sims,
                    int32_t s_max, rtgpu_sim_out *out);
 
 /* Device path: every pointer (including those inside *out) is device
- * memory; scratch holds sum of rtgpu_sim_scratch_words at scr_off[s]. */
+ * memory; scratch holds sum of rtgpu_sim_scratch_words at scr_off[s].
+ * order (may be NULL): a permutation of the simulations, started in that
+ * order -- longest first (e.g. by event capacity) list-schedules the batch. */
 int rtgpu_sim_device(const int64_t *blobs, const int64_t *set_off, int64_t n_sims,
                      const int64_t *job_base, const int64_t *task_base, const int64_t *ev_base,
-                     const int64_t *scr_off, int64_t *scratch, int32_t s_max,
-                     const rtgpu_sim_out *out, void *stream);
+                     const int64_t *scr_off, int64_t *scratch, const int64_t *order,
+                     int32_t s_max, const rtgpu_sim_out *out, void *stream);
 
 const char *rtgpu_sim_last_error(void);
 

@@ -15,12 +15,15 @@
  * threads, no shared memory) so exiting blocks of other tasks always find
  * room on an occupied SM and cannot delay a partition.
  */
+#include <cuda.h> /* types of the driver entry point fetched at run time */
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
 
+#include <dirent.h>
 #include <pthread.h>
+#include <stdlib.h>
 #include <sched.h>
 #include <time.h>
 
@@ -100,7 +103,6 @@ __device__ __forceinline__ unsigned gadd32(unsigned *p, unsigned v) {
  * partitions, and must not steal their issue slots. */
 __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
     __shared__ unsigned slot;
-    __shared__ unsigned long long item;
     const unsigned sm = smid();
     if (!((a.mask[sm >> 5] >> (sm & 31)) & 1u)) return;
     const unsigned long long t_in = gtimer();
@@ -121,20 +123,25 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
     /* synthetic compute work: three dependent FMA chains per thread, so one
      * block (one warp per SM sub-partition) keeps the FMA pipe ~3/4 busy and
      * the second slot's block fills the rest: interleave ratio
-     * alpha = 2 t2 / t1 ~ 1.5, inside the model's [1, 1.8] (model.py:17).
-     * The next item is claimed before the current one is computed and its
-     * value is only consumed after the FMA loop, so the atomic's round trip
-     * (L2-die and load dependent) never sits on the item's critical path. */
+     * alpha = 2 t2 / t1 ~ 1.3-1.5, inside the model's [1, 1.8] (model.py:17).
+     * Every WARP claims its own work items (a segment's `items` are block
+     * items of blockDim/32 warp items each): no block-wide barrier per item,
+     * so a warp slowed by an unlucky sub-partition placement (the warp slots
+     * exiting blocks of other grids leave behind) costs only its own share
+     * and the others absorb the rest.  The next item is claimed before the
+     * current one is computed and only consumed after it, so the atomic's
+     * round trip never sits on the critical path. */
+    const int lane = threadIdx.x & 31;
+    const long long witems = a.items * (long long)(blockDim.x >> 5);
     float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f;
-    __shared__ unsigned long long next;
-    if (threadIdx.x == 0) item = claim(&a.ctl->work);
-    __syncthreads();
-    unsigned long long it = item;
+    unsigned long long it = 0;
+    if (lane == 0) it = claim(&a.ctl->work);
+    it = __shfl_sync(0xffffffffu, it, 0);
     unsigned done = 0;
-    while ((long long)it < a.items) {
+    while ((long long)it < witems) {
         done++;
         unsigned long long nx = 0;
-        if (threadIdx.x == 0) nx = claim(&a.ctl->work); /* in flight during the loop */
+        if (lane == 0) nx = claim(&a.ctl->work); /* in flight during the loop */
         const int iters = a.iters;
 #pragma unroll 4
         for (int k = 0; k < iters; k++) {
@@ -142,11 +149,9 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
             x1 = fmaf(x1, 0.9999999f, 0.5f);
             x2 = fmaf(x2, 0.9999999f, 0.5f);
         }
-        if (threadIdx.x == 0) next = nx;
-        __syncthreads();
-        it = next;
-        __syncthreads();
+        it = __shfl_sync(0xffffffffu, nx, 0);
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         gmax(&a.ctl->end, gtimer());
         if (tpos < 16) a.ctl->bitems[tpos] = done;
@@ -176,6 +181,13 @@ struct Lane {
     cudaEvent_t k0[RING] = {}, k1[RING] = {};
     cudaEvent_t ev_wait = nullptr; /* blocking-sync: a waiting thread sleeps */
     bool spin = false;             /* waits poll instead of sleeping (own core) */
+    /* completion flag: the stream writes `seq` into pinned host memory
+     * (cuStreamWriteValue32), so a polling thread makes no CUDA call --
+     * polling cudaEventQuery from several threads contends on the driver
+     * lock and delays the other tasks' launches */
+    volatile uint32_t *hflag = nullptr;
+    CUdeviceptr dflag = 0;
+    uint32_t seq = 0;
     void use(int k) {
         ctl = ring + k;
         hctl = hring + k;
@@ -187,6 +199,23 @@ int sm_count() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
+}
+
+typedef CUresult (*WriteValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+WriteValue32 write_value32() {
+    static WriteValue32 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (WriteValue32)p;
+        cudaGetLastError();
+    }
+    return fn;
 }
 
 int lane_init(Lane &L, size_t buf) {
@@ -207,6 +236,18 @@ int lane_init(Lane &L, size_t buf) {
         cudaEventCreate(&L.k1[k]);
     }
     cudaEventCreateWithFlags(&L.ev_wait, cudaEventBlockingSync | cudaEventDisableTiming);
+    void *hf = nullptr;
+    if (write_value32() && cudaHostAlloc(&hf, 64, cudaHostAllocMapped) == cudaSuccess) {
+        void *df = nullptr;
+        if (cudaHostGetDevicePointer(&df, hf, 0) == cudaSuccess) {
+            L.hflag = (volatile uint32_t *)hf;
+            *L.hflag = 0;
+            L.dflag = (CUdeviceptr)df;
+        } else {
+            cudaFreeHost(hf);
+        }
+    }
+    cudaGetLastError();
     return 0;
 }
 
@@ -225,11 +266,20 @@ void lane_free(Lane &L) {
         if (L.k1[k]) cudaEventDestroy(L.k1[k]);
     }
     if (L.ev_wait) cudaEventDestroy(L.ev_wait);
+    if (L.hflag) cudaFreeHost((void *)L.hflag);
 }
 
 /* wait for the lane's stream: poll when the thread owns its core (no
  * wake-up latency), else sleep so lower-priority threads on the core run */
 void lane_wait(Lane &L) {
+    if (L.spin && L.hflag) {
+        const uint32_t want = ++L.seq;
+        if (write_value32()((CUstream)L.st, L.dflag, want, CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS) {
+            while (*L.hflag != want) {
+            }
+            return;
+        }
+    }
     cudaEventRecord(L.ev_wait, L.st);
     if (L.spin) {
         while (cudaEventQuery(L.ev_wait) == cudaErrorNotReady) {
@@ -352,6 +402,38 @@ std::vector<int> allowed_cpus() {
     return out;
 }
 
+/* Keep every other thread of the process (the caller, the CUDA driver's
+ * helpers) off the task threads' cores for the run, so a polling task
+ * thread is never time-sliced away; restore() puts the old masks back. */
+struct CoreFence {
+    std::vector<std::pair<pid_t, cpu_set_t>> saved;
+    void apply(const std::vector<int> &reserved, const std::vector<int> &all) {
+        cpu_set_t others;
+        CPU_ZERO(&others);
+        int n_others = 0;
+        for (int c : all)
+            if (std::find(reserved.begin(), reserved.end(), c) == reserved.end()) {
+                CPU_SET(c, &others);
+                n_others++;
+            }
+        if (n_others == 0) return;
+        DIR *d = opendir("/proc/self/task");
+        if (!d) return;
+        while (dirent *e = readdir(d)) {
+            const pid_t tid = (pid_t)atoi(e->d_name);
+            if (tid <= 0) continue;
+            cpu_set_t old;
+            if (sched_getaffinity(tid, sizeof old, &old) != 0) continue;
+            if (sched_setaffinity(tid, sizeof others, &others) == 0) saved.push_back({tid, old});
+        }
+        closedir(d);
+    }
+    void restore() {
+        for (auto &x : saved) sched_setaffinity(x.first, sizeof x.second, &x.second);
+        saved.clear();
+    }
+};
+
 bool pin_thread(int cpu) {
     cpu_set_t set;
     CPU_ZERO(&set);
@@ -426,7 +508,7 @@ int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items,
         }
     }
     if (loaded) {
-        const unsigned long long stop = (unsigned long long)1 << 41;
+        const unsigned long long stop = (unsigned long long)1 << 62; /* past any segment's warp items */
         cudaMemcpy(&B.ctl->work, &stop, sizeof stop, cudaMemcpyHostToDevice);
         cudaStreamSynchronize(B.st);
         lane_free(B);
@@ -523,7 +605,7 @@ int rtgpu_exec_probe(const uint32_t *mask, int nslots, int64_t items, int iters,
     stop = true;
     bg.join();
     if (load == 3) {
-        const unsigned long long stopw = (unsigned long long)1 << 41;
+        const unsigned long long stopw = (unsigned long long)1 << 62; /* past any segment's warp items */
         cudaMemcpy(&B.ctl->work, &stopw, sizeof stopw, cudaMemcpyHostToDevice);
     }
     cudaDeviceSynchronize();
@@ -582,6 +664,9 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
     const int cpu_mode = g_cpu_mode, bus_mode = g_bus_mode;
     std::atomic<int> fifo_fail{0};
     Bus bus;
+    CoreFence fence;
+    if (cpu_mode == RTGPU_EXEC_CPU_PARALLEL && (int)cpus.size() > n_tasks)
+        fence.apply(std::vector<int>(cpus.begin(), cpus.begin() + n_tasks), cpus);
     auto t_start = clk::now() + std::chrono::milliseconds(50);
     std::vector<std::thread> th;
     for (int i = 0; i < n_tasks; i++) {
@@ -688,6 +773,7 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
         });
     }
     for (auto &x : th) x.join();
+    fence.restore();
     for (int i = 0; i < n_tasks; i++) {
         results[i].cpu_mode = (cpu_mode == RTGPU_EXEC_CPU_FP_ONE_CORE && fifo_fail == 0)
                                   ? RTGPU_EXEC_CPU_FP_ONE_CORE : RTGPU_EXEC_CPU_PARALLEL;

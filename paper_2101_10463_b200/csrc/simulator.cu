@@ -28,6 +28,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -38,15 +39,20 @@ namespace {
 typedef int64_t i64;
 
 constexpr int JW0 = 12; /* job record: fixed fields before lens[] / segr[] */
-enum { J_TASK = 0, J_K, J_REL, J_DL, J_POS, J_REM, J_DONE, J_GFIN, J_GSEQ, J_S };
+/* J_SLOT: the job's output slot (release order); J_DLP: its deadline event
+ * is still pending (the record is recycled once done and past it) */
+enum { J_TASK = 0, J_K, J_REL, J_DL, J_POS, J_REM, J_DONE, J_GFIN, J_GSEQ, J_S, J_SLOT, J_DLP };
 
 __host__ __device__ inline i64 job_words(int s_max) { return JW0 + 2 * (i64)s_max; }
 
+/* job-record pool: header [8] records (0: one per release point) */
+__host__ __device__ inline i64 pool_of(const i64 *b) { return b[8] > 0 && b[8] < b[3] ? b[8] : b[3]; }
+
 __host__ __device__ inline i64 scratch_words(const i64 *b) {
-    const i64 R = b[3], smax = b[6];
-    /* jobs, three queues (cpu, bus, gpu), per-task state (4 x 64),
-     * MT19937 state (624 x u32 + index) */
-    return R * job_words((int)smax) + 3 * R + 4 * RTGPU_SIM_MAX_TASKS + 320;
+    const i64 P = pool_of(b), smax = b[6];
+    /* job records, three queues (cpu, bus, gpu) and the free stack (int32),
+     * per-task state (4 x 64), MT19937 state (624 x u32 + index) */
+    return P * job_words((int)smax) + 2 * P + 2 + 4 * RTGPU_SIM_MAX_TASKS + 320;
 }
 
 /* ------------------------------------------------------------ MT19937 */
@@ -117,14 +123,32 @@ struct MT {
 
 /* ------------------------------------------------------------ simulation */
 
+/* One warp per simulation.  Every lane runs the same (warp-uniform) event
+ * loop on the same state -- no divergence -- and the scans are lane-
+ * parallel: task t's next release and pending deadline live in the
+ * registers of lane t % 32 (two per lane: tasks t and t + 32), the next
+ * event is a butterfly min over lanes, ready queues and the GPU set are
+ * scanned 32 entries at a time.  Job records live in a recycled pool in
+ * global scratch (L1-resident for the live jobs); all lanes store the same
+ * values, so each lane reads its own writes without synchronisation. */
+constexpr i64 INF = 0x7fffffffffffffffLL;
+
+__device__ __forceinline__ i64 shfl64(i64 v, int m) { return (i64)__shfl_xor_sync(0xffffffffu, (long long)v, m); }
+
 struct Sim {
     const i64 *blob, *tr;
-    int n, policy, smax, jw, sstride; /* sstride: seg_max row width */
+    int n, policy, smax, jw, sstride, lane; /* sstride: seg_max row width */
     i64 H, R, evcap;
     i64 *jobs;
-    int *cq, *bq, *gq;
-    int cn, bn, gn;
-    i64 *next_k, *dl_time, *dl_seq, *dl_job;
+    int *cq, *bq, *gq, *freel;
+    int cn, bn, gn, fn;
+    bool pool_out;
+    /* lane-held state of tasks a = lane and b = lane + 32 */
+    i64 TA, TB, DA, DB;      /* period, relative deadline        */
+    i64 relA, relB;          /* next release time (INF: none)    */
+    i64 kA, kB;              /* next job index                   */
+    i64 dlA, dlB, dsA, dsB;  /* pending deadline: time, seq      */
+    int djA, djB;            /* its job record (-1: none)        */
     MT rng;
     int cpu_run, bus_run;
     i64 run_fin, run_seq, bus_fin, bus_seq;
@@ -144,7 +168,7 @@ struct Sim {
 
     __device__ void emit(i64 time, int j, int kind, int seg, int action) {
         if (nev < evcap) {
-            if (ev) {
+            if (ev && lane == 0) {
                 const i64 *jr = J(j);
                 ev[nev].time = time;
                 ev[nev].packed = (uint64_t)(uint32_t)jr[J_K] | ((uint64_t)(jr[J_TASK] & 0xff) << 32) |
@@ -158,25 +182,34 @@ struct Sim {
     }
     __device__ i64 &seg_start(int j, int pos) { return J(j)[JW0 + smax + pos]; }
 
-    /* first index of the best priority (lowest task index) in a queue */
+    /* first index of the best priority (lowest task index) in a queue:
+     * warp min of (task, position) */
     __device__ int best_in(const int *q, int cnt) const {
-        int bi = 0;
-        i64 bt = J(q[0])[J_TASK];
-        for (int x = 1; x < cnt; x++) {
-            const i64 t = J(q[x])[J_TASK];
-            if (t < bt) {
-                bt = t;
-                bi = x;
-            }
+        int best = 0x7fffffff;
+        for (int x = lane; x < cnt; x += 32) {
+            const int key = ((int)J(q[x])[J_TASK] << 20) | x;
+            best = key < best ? key : best;
         }
-        return bi;
+        for (int m = 16; m; m >>= 1) {
+            const int o = __shfl_xor_sync(0xffffffffu, best, m);
+            best = o < best ? o : best;
+        }
+        return best & 0xfffff;
     }
-    __device__ static void remove_at(int *q, int &cnt, int at) {
-        for (int x = at; x + 1 < cnt; x++) q[x] = q[x + 1];
+    /* order-preserving removal (ties among one task's jobs keep FIFO order) */
+    __device__ void remove_at(int *q, int &cnt, int at) const {
+        for (int base = at; base + 1 < cnt; base += 32) {
+            const int x = base + lane;
+            const int v = x + 1 < cnt ? q[x + 1] : 0;
+            __syncwarp();
+            if (x + 1 < cnt) q[x] = v;
+            __syncwarp();
+        }
         cnt--;
     }
 
     __device__ void start_cpu(i64 time, int j, bool resumed) {
+        __syncwarp();
         i64 *jr = J(j);
         cpu_run = j;
         const i64 *e = plan((int)jr[J_TASK], (int)jr[J_POS]);
@@ -201,9 +234,12 @@ struct Sim {
         } else if (J(top)[J_TASK] < J(cpu_run)[J_TASK]) {
             const int v = cpu_run;
             i64 *vr = J(v);
+            __syncwarp();
             vr[J_REM] = run_fin - time;
             emit(time, v, RTGPU_KIND_CPU, idx_of(plan((int)vr[J_TASK], (int)vr[J_POS])), RTGPU_EV_PREEMPT);
+            __syncwarp();
             cq[cn++] = v;
+            __syncwarp();
             remove_at(cq, cn, t);
             cpu_run = -1;
             start_cpu(time, top, J(top)[J_REM] != cur_dur(top));
@@ -224,46 +260,68 @@ struct Sim {
     }
 
     __device__ void dispatch(i64 time, int j) {
+        __syncwarp();
         i64 *jr = J(j);
         const int pos = (int)jr[J_POS];
         const i64 *e = plan((int)jr[J_TASK], pos);
         const int kind = kind_of(e);
         if (kind == RTGPU_KIND_CPU) {
             jr[J_REM] = cur_dur(j);
+            __syncwarp();
             cq[cn++] = j;
+            __syncwarp();
             sched_cpu(time);
         } else if (kind == RTGPU_KIND_MEM) {
+            __syncwarp();
             bq[bn++] = j;
+            __syncwarp();
             grant_bus(time);
         } else { /* dedicated virtual SMs: starts at once */
             emit(time, j, RTGPU_KIND_GPU, idx_of(e), RTGPU_EV_START);
             if (seg_start(j, pos) < 0) seg_start(j, pos) = time;
             jr[J_GFIN] = time + cur_dur(j);
             jr[J_GSEQ] = seq++;
+            __syncwarp();
             gq[gn++] = j;
+            __syncwarp();
         }
     }
 
     __device__ void advance(i64 time, int j) {
+        __syncwarp();
         i64 *jr = J(j);
         const int task = (int)jr[J_TASK];
         const int pos = (int)jr[J_POS];
         const i64 *e = plan(task, pos);
         emit(time, j, kind_of(e), idx_of(e), RTGPU_EV_FINISH);
-        seg_start(j, pos) = time - seg_start(j, pos); /* start -> finish response */
+        const i64 st0 = seg_start(j, pos);
+        __syncwarp(); /* every lane has read the record before any rewrites it */
+        seg_start(j, pos) = time - st0; /* start -> finish response */
         jr[J_POS] = pos + 1;
         if (pos + 1 == (int)jr[J_S]) {
             jr[J_DONE] = 1;
             const i64 resp = time - jr[J_REL];
-            job_resp[j] = resp;
-            job_rank[j] = (int32_t)rank++;
+            if (lane == 0) {
+                job_resp[jr[J_SLOT]] = resp;
+                job_rank[jr[J_SLOT]] = (int32_t)rank;
+            }
+            rank++;
             if (time > jr[J_DL]) {
                 emit(time, j, RTGPU_KIND_JOB, -1, RTGPU_EV_DEADLINE_MISS);
                 misses++;
             }
+            __syncwarp();
             i64 *sm = seg_max + (i64)task * sstride;
-            for (int p = 0; p < (int)jr[J_S]; p++) sm[p] = sm[p] > seg_start(j, p) ? sm[p] : seg_start(j, p);
-            if (resp > resp_max[task]) resp_max[task] = resp;
+            for (int p = lane; p < (int)jr[J_S]; p += 32) {
+                const i64 v = seg_start(j, p);
+                if (v > sm[p]) sm[p] = v;
+            }
+            if (lane == 0 && resp > resp_max[task]) resp_max[task] = resp;
+            __syncwarp();
+            if (!jr[J_DLP]) {
+                freel[fn++] = j;
+                __syncwarp();
+            }
         } else {
             dispatch(time, j);
         }
@@ -271,62 +329,114 @@ struct Sim {
 
     __device__ void release(i64 time, int task) {
         const i64 *t = tr + task * RTGPU_SIM_TASK;
-        const int j = (int)n_jobs++;
+        if (fn == 0) { /* more live jobs than the pool holds: the host re-runs */
+            pool_out = true;
+            return;
+        }
+        const int j = freel[--fn];
+        const i64 slot = n_jobs++;
         i64 *jr = J(j);
         const int S = (int)t[0];
+        const bool mine = lane == (task & 31), hi = task >= 32;
+        const i64 k = hi ? kB : kA; /* valid in the owning lane */
+        const i64 kk = (i64)__shfl_sync(0xffffffffu, (long long)k, task & 31);
+        if (mine) {
+            if (hi) {
+                kB++;
+                relB = kB * TB < H ? kB * TB : INF;
+            } else {
+                kA++;
+                relA = kA * TA < H ? kA * TA : INF;
+            }
+        }
+        jr[J_SLOT] = slot;
+        jr[J_DLP] = 1;
         jr[J_TASK] = task;
-        jr[J_K] = next_k[task]++;
+        jr[J_K] = kk;
         jr[J_REL] = time;
         jr[J_DL] = time + t[2];
         jr[J_POS] = 0;
         jr[J_REM] = 0;
         jr[J_DONE] = 0;
         jr[J_S] = S;
-        for (int p = 0; p < S; p++) {
-            const i64 *e = plan(task, p);
-            i64 d = e[3];
-            if (policy == 1 && ((e[0] >> 16) & 1)) d = rng.randint(e[1], e[2]) * e[4] + e[5];
-            jr[JW0 + p] = d;
+        __syncwarp();
+        for (int p = lane; p < S; p += 32) { /* fixed lengths, in parallel */
+            jr[JW0 + p] = plan(task, p)[3];
             seg_start(j, p) = -1;
         }
-        job_task[j] = task;
-        job_k[j] = (int32_t)jr[J_K];
-        job_resp[j] = -1;
-        job_rank[j] = -1;
+        __syncwarp();
+        if (policy == 1) /* draws in plan order, one stream, lane 0's generator */
+            for (int p = 0; p < S; p++) {
+                const i64 *e = plan(task, p);
+                if ((e[0] >> 16) & 1) {
+                    i64 d = 0;
+                    if (lane == 0) d = rng.randint(e[1], e[2]) * e[4] + e[5];
+                    d = (i64)__shfl_sync(0xffffffffu, (long long)d, 0);
+                    jr[JW0 + p] = d;
+                }
+            }
+        __syncwarp();
+        if (lane == 0) {
+            job_task[slot] = task;
+            job_k[slot] = (int32_t)kk;
+            job_resp[slot] = -1;
+            job_rank[slot] = -1;
+        }
         emit(time, j, RTGPU_KIND_JOB, -1, RTGPU_EV_RELEASE);
-        dl_time[task] = jr[J_DL];
-        dl_seq[task] = seq++;
-        dl_job[task] = j;
+        const i64 dseq = seq++;
+        if (mine) {
+            if (hi) {
+                dlB = jr[J_DL];
+                dsB = dseq;
+                djB = j;
+            } else {
+                dlA = jr[J_DL];
+                dsA = dseq;
+                djA = j;
+            }
+        }
         dispatch(time, j);
     }
 
     __device__ void run() {
         for (;;) {
-            /* next event: lexicographic min of (time, order, seq) */
-            int type = -1, arg = -1;
-            i64 bt = 0, bs = 0;
-            int bo = 9;
-            auto consider = [&](i64 t, int o, i64 s, int ty, int a) {
-                if (type < 0 || t < bt || (t == bt && (o < bo || (o == bo && s < bs)))) {
+            /* next event: lexicographic min of (time, order << 58 | seq) over
+             * lanes (GPU finishes, deadlines, releases), then the CPU and bus
+             * finishes every lane holds */
+            i64 bt = INF, bk = INF;
+            int bp = -1; /* type << 16 | arg */
+            auto consider = [&](i64 t, i64 key, int p) {
+                if (t < bt || (t == bt && key < bk)) {
                     bt = t;
-                    bo = o;
-                    bs = s;
-                    type = ty;
-                    arg = a;
+                    bk = key;
+                    bp = p;
                 }
             };
-            if (cpu_run >= 0) consider(run_fin, 0, run_seq, 0, cpu_run);
-            if (bus_run >= 0) consider(bus_fin, 0, bus_seq, 1, bus_run);
-            for (int x = 0; x < gn; x++) {
+            for (int x = lane; x < gn; x += 32) {
                 const i64 *jr = J(gq[x]);
-                consider(jr[J_GFIN], 0, jr[J_GSEQ], 2, x);
+                consider(jr[J_GFIN], jr[J_GSEQ], (2 << 16) | x);
             }
-            for (int i = 0; i < n; i++) {
-                if (dl_job[i] >= 0) consider(dl_time[i], 1, dl_seq[i], 3, i);
-                const i64 rt = next_k[i] * tr[i * RTGPU_SIM_TASK + 1];
-                if (rt < H) consider(rt, 2, i, 4, i);
+            if (lane < n) {
+                if (djA >= 0) consider(dlA, ((i64)1 << 58) | dsA, (3 << 16) | lane);
+                if (relA != INF) consider(relA, ((i64)2 << 58) | lane, (4 << 16) | lane);
             }
-            if (type < 0 || bt > H) break;
+            if (lane + 32 < n) {
+                if (djB >= 0) consider(dlB, ((i64)1 << 58) | dsB, (3 << 16) | (lane + 32));
+                if (relB != INF) consider(relB, ((i64)2 << 58) | (lane + 32), (4 << 16) | (lane + 32));
+            }
+            for (int m = 16; m; m >>= 1) {
+                const i64 t2 = shfl64(bt, m), k2 = shfl64(bk, m);
+                const int p2 = __shfl_xor_sync(0xffffffffu, bp, m);
+                if (t2 < bt || (t2 == bt && k2 < bk)) {
+                    bt = t2;
+                    bk = k2;
+                    bp = p2;
+                }
+            }
+            if (cpu_run >= 0) consider(run_fin, run_seq, 0);
+            if (bus_run >= 0) consider(bus_fin, bus_seq, 1 << 16);
+            if (bp < 0 || bt > H) break;
+            const int type = bp >> 16, arg = bp & 0xffff;
             if (type == 0) {
                 const int j = cpu_run;
                 cpu_run = -1;
@@ -339,29 +449,49 @@ struct Sim {
                 grant_bus(bt);
             } else if (type == 2) {
                 const int j = gq[arg];
-                remove_at(gq, gn, arg);
+                __syncwarp();
+                gq[arg] = gq[gn - 1]; /* the GPU set is unordered: ties use seq */
+                gn--;
+                __syncwarp();
                 advance(bt, j);
             } else if (type == 3) {
-                const int j = (int)dl_job[arg];
-                dl_job[arg] = -1;
+                const bool hi = arg >= 32;
+                const int j = __shfl_sync(0xffffffffu, hi ? djB : djA, arg & 31);
+                if (lane == (arg & 31)) {
+                    if (hi) djB = -1;
+                    else djA = -1;
+                }
+                J(j)[J_DLP] = 0;
                 if (!J(j)[J_DONE]) {
                     emit(bt, j, RTGPU_KIND_JOB, -1, RTGPU_EV_DEADLINE_MISS);
                     misses++;
+                } else {
+                    __syncwarp();
+                    freel[fn++] = j;
+                    __syncwarp();
                 }
             } else {
                 release(bt, arg);
+                if (pool_out) break;
             }
         }
     }
 };
 
-__global__ void __launch_bounds__(128) sim_kernel(const i64 *blobs, const i64 *set_off, i64 n_sims,
-                                                  const i64 *job_base, const i64 *task_base,
-                                                  const i64 *ev_base, const i64 *scr_off, i64 *scratch,
-                                                  int s_max_out, rtgpu_sim_out o) {
-    for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < n_sims; s += (i64)gridDim.x * blockDim.x) {
+/* One single-warp block per simulation: the block scheduler hands blocks to
+ * SMs as they free up, so with `order` = longest-first (the host's estimate
+ * from release points x plan length) the batch is list-scheduled and the
+ * longest simulations do not start last. */
+__global__ void __launch_bounds__(32) sim_kernel(const i64 *blobs, const i64 *set_off, i64 n_sims,
+                                                 const i64 *job_base, const i64 *task_base,
+                                                 const i64 *ev_base, const i64 *scr_off, i64 *scratch,
+                                                 const i64 *order, int s_max_out, rtgpu_sim_out o) {
+    const int lane = threadIdx.x & 31;
+    {
+        const i64 s = order ? order[blockIdx.x] : (i64)blockIdx.x;
         const i64 *b = blobs + set_off[s];
         Sim m;
+        m.lane = lane;
         m.blob = b;
         m.n = (int)b[0];
         m.policy = (int)b[1];
@@ -376,32 +506,45 @@ __global__ void __launch_bounds__(128) sim_kernel(const i64 *blobs, const i64 *s
         if (m.n < 0 || m.n > RTGPU_SIM_MAX_TASKS || m.smax > s_max_out || m.R != job_base[s + 1] - jb ||
             task_base[s + 1] - tb != m.n || (m.policy == 1 && (b[5] < 1 || b[5] > RTGPU_SIM_MAX_KEY)))
             st = RTGPU_SIM_BAD_INPUT;
-        o.n_events[s] = 0;
-        o.misses[s] = 0;
         if (st != RTGPU_SIM_OK) {
-            o.status[s] = st;
-            continue;
+            if (lane == 0) {
+                o.n_events[s] = 0;
+                o.misses[s] = 0;
+                o.status[s] = st;
+            }
+            return;
         }
+        const i64 P = pool_of(b);
         i64 *w = scratch + scr_off[s];
         m.jobs = w;
-        w += m.R * m.jw;
+        w += P * m.jw;
         m.cq = (int *)w;
-        m.bq = m.cq + m.R;
-        m.gq = m.bq + m.R;
-        w += (3 * m.R + 1) / 2 + 1;
-        m.next_k = w;
-        m.dl_time = w + RTGPU_SIM_MAX_TASKS;
-        m.dl_seq = w + 2 * RTGPU_SIM_MAX_TASKS;
-        m.dl_job = w + 3 * RTGPU_SIM_MAX_TASKS;
+        m.bq = m.cq + P;
+        m.gq = m.bq + P;
+        m.freel = m.gq + P;
+        w += 2 * P + 2;
+        for (i64 x = lane; x < P; x += 32) m.freel[x] = (int)(P - 1 - x);
+        m.fn = (int)P;
+        m.pool_out = false;
         w += 4 * RTGPU_SIM_MAX_TASKS;
         m.rng.mt = (uint32_t *)w;
-        if (m.policy == 1) m.rng.init_by_array(b + b[7], (int)b[5]);
-        for (int i = 0; i < m.n; i++) {
-            m.next_k[i] = 0;
-            m.dl_job[i] = -1;
+        if (m.policy == 1 && lane == 0) m.rng.init_by_array(b + b[7], (int)b[5]);
+        __syncwarp();
+        const int ta = lane, tbb = lane + 32;
+        m.TA = ta < m.n ? m.tr[ta * RTGPU_SIM_TASK + 1] : 1;
+        m.DA = ta < m.n ? m.tr[ta * RTGPU_SIM_TASK + 2] : 0;
+        m.TB = tbb < m.n ? m.tr[tbb * RTGPU_SIM_TASK + 1] : 1;
+        m.DB = tbb < m.n ? m.tr[tbb * RTGPU_SIM_TASK + 2] : 0;
+        m.kA = m.kB = 0;
+        m.relA = (ta < m.n && 0 < m.H) ? 0 : INF;
+        m.relB = (tbb < m.n && 0 < m.H) ? 0 : INF;
+        m.djA = m.djB = -1;
+        m.dlA = m.dlB = m.dsA = m.dsB = 0;
+        for (int i = lane; i < m.n; i += 32) {
             o.resp_max[tb + i] = -1;
             for (int p = 0; p < s_max_out; p++) o.seg_max[(tb + i) * s_max_out + p] = -1;
         }
+        __syncwarp();
         m.cn = m.bn = m.gn = 0;
         m.cpu_run = m.bus_run = -1;
         m.run_fin = m.run_seq = m.bus_fin = m.bus_seq = 0;
@@ -417,9 +560,13 @@ __global__ void __launch_bounds__(128) sim_kernel(const i64 *blobs, const i64 *s
         m.sstride = s_max_out;
         m.resp_max = o.resp_max + tb;
         m.run();
-        o.status[s] = m.overflow ? RTGPU_SIM_EVENT_OVERFLOW : RTGPU_SIM_OK;
-        o.n_events[s] = m.nev;
-        o.misses[s] = m.misses;
+        __syncwarp();
+        if (lane == 0) {
+            o.status[s] = m.pool_out ? RTGPU_SIM_POOL_OVERFLOW
+                                     : (m.overflow ? RTGPU_SIM_EVENT_OVERFLOW : RTGPU_SIM_OK);
+            o.n_events[s] = m.nev;
+            o.misses[s] = m.misses;
+        }
     }
 }
 
@@ -427,16 +574,15 @@ char g_err[256] = "";
 std::mutex g_mu;
 
 int launch(const i64 *blobs, const i64 *set_off, i64 n_sims, const i64 *job_base, const i64 *task_base,
-           const i64 *ev_base, const i64 *scr_off, i64 *scratch, int s_max, const rtgpu_sim_out &o,
-           cudaStream_t st) {
+           const i64 *ev_base, const i64 *scr_off, i64 *scratch, const i64 *order, int s_max,
+           const rtgpu_sim_out &o, cudaStream_t st) {
     if (n_sims <= 0) return 0;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    i64 grid = (n_sims + 127) / 128;
-    if (grid > (i64)sms * 16) grid = (i64)sms * 16;
-    sim_kernel<<<(unsigned)grid, 128, 0, st>>>(blobs, set_off, n_sims, job_base, task_base, ev_base, scr_off,
-                                               scratch, s_max, o);
+    if (n_sims > 0x7fffffffLL) {
+        snprintf(g_err, sizeof g_err, "too many simulations in one launch");
+        return -3;
+    }
+    sim_kernel<<<(unsigned)n_sims, 32, 0, st>>>(blobs, set_off, n_sims, job_base, task_base, ev_base, scr_off,
+                                               scratch, order, s_max, o);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         snprintf(g_err, sizeof g_err, "sim_kernel launch: %s", cudaGetErrorString(e));
@@ -455,10 +601,11 @@ int64_t rtgpu_sim_scratch_words(const int64_t *blob) { return scratch_words((con
 
 int rtgpu_sim_device(const int64_t *blobs, const int64_t *set_off, int64_t n_sims, const int64_t *job_base,
                      const int64_t *task_base, const int64_t *ev_base, const int64_t *scr_off,
-                     int64_t *scratch, int32_t s_max, const rtgpu_sim_out *out, void *stream) {
+                     int64_t *scratch, const int64_t *order, int32_t s_max, const rtgpu_sim_out *out,
+                     void *stream) {
     return launch((const i64 *)blobs, (const i64 *)set_off, n_sims, (const i64 *)job_base,
-                  (const i64 *)task_base, (const i64 *)ev_base, (const i64 *)scr_off, (i64 *)scratch, s_max,
-                  *out, (cudaStream_t)stream);
+                  (const i64 *)task_base, (const i64 *)ev_base, (const i64 *)scr_off, (i64 *)scratch,
+                  (const i64 *)order, s_max, *out, (cudaStream_t)stream);
 }
 
 int rtgpu_sim_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sims, const int64_t *job_base,
@@ -467,12 +614,16 @@ int rtgpu_sim_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sims,
     if (n_sims <= 0) return 0;
     const i64 W = set_off[n_sims], NJ = job_base[n_sims], NT = task_base[n_sims];
     const i64 NE = (out->events && ev_base) ? ev_base[n_sims] : 0;
-    std::vector<i64> scr(n_sims + 1, 0);
+    std::vector<i64> scr(n_sims + 1, 0), order(n_sims);
     for (i64 s = 0; s < n_sims; s++) scr[s + 1] = scr[s] + scratch_words((const i64 *)blobs + set_off[s]);
+    for (i64 s = 0; s < n_sims; s++) order[s] = s;
+    std::stable_sort(order.begin(), order.end(), [&](i64 a, i64 b) {
+        return blobs[set_off[a] + 4] > blobs[set_off[b] + 4]; /* event capacity: longest first */
+    });
     struct Buf {
         void *p = nullptr;
         ~Buf() { cudaFree(p); }
-    } d_blob, d_off, d_jb, d_tb, d_eb, d_scro, d_scr, d_out;
+    } d_blob, d_off, d_jb, d_tb, d_eb, d_scro, d_scr, d_out, d_ord;
     const size_t n1 = (size_t)(n_sims + 1) * 8;
     size_t out_bytes = 0;
     const size_t o_status = out_bytes;
@@ -497,7 +648,8 @@ int rtgpu_sim_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sims,
     out_bytes += (size_t)NE * sizeof(rtgpu_sim_event);
     if (cudaMalloc(&d_blob.p, (size_t)W * 8 + 8) || cudaMalloc(&d_off.p, n1) || cudaMalloc(&d_jb.p, n1) ||
         cudaMalloc(&d_tb.p, n1) || cudaMalloc(&d_eb.p, n1) || cudaMalloc(&d_scro.p, n1) ||
-        cudaMalloc(&d_scr.p, (size_t)scr[n_sims] * 8 + 8) || cudaMalloc(&d_out.p, out_bytes + 8)) {
+        cudaMalloc(&d_scr.p, (size_t)scr[n_sims] * 8 + 8) || cudaMalloc(&d_out.p, out_bytes + 8) ||
+        cudaMalloc(&d_ord.p, (size_t)n_sims * 8)) {
         snprintf(g_err, sizeof g_err, "cudaMalloc: %s", cudaGetErrorString(cudaGetLastError()));
         return -6;
     }
@@ -507,6 +659,7 @@ int rtgpu_sim_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sims,
     cudaMemcpy(d_tb.p, task_base, n1, cudaMemcpyHostToDevice);
     if (NE) cudaMemcpy(d_eb.p, ev_base, n1, cudaMemcpyHostToDevice);
     cudaMemcpy(d_scro.p, scr.data(), n1, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_ord.p, order.data(), (size_t)n_sims * 8, cudaMemcpyHostToDevice);
     char *ob = (char *)d_out.p;
     rtgpu_sim_out d;
     d.status = (int32_t *)(ob + o_status);
@@ -521,7 +674,7 @@ int rtgpu_sim_host(const int64_t *blobs, const int64_t *set_off, int64_t n_sims,
     d.events = NE ? (rtgpu_sim_event *)(ob + o_ev) : nullptr;
     int rc = launch((const i64 *)d_blob.p, (const i64 *)d_off.p, n_sims, (const i64 *)d_jb.p,
                     (const i64 *)d_tb.p, NE ? (const i64 *)d_eb.p : nullptr, (const i64 *)d_scro.p,
-                    (i64 *)d_scr.p, s_max, d, 0);
+                    (i64 *)d_scr.p, (const i64 *)d_ord.p, s_max, d, 0);
     if (rc) return rc;
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {

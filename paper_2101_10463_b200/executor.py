@@ -182,7 +182,15 @@ def _ceil_margin(x_us: float, margin: float) -> int:
 CAL_SMS = (0, 74)  # one SM on each die: L2 distance differs per die
 
 
-def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = 0.12,
+# Safety margin on measured worst cases.  A kernel's speed on its SMs depends
+# on how its warps land on the four SM sub-partitions (the warp slots other
+# grids' exiting blocks leave free): with two 4-warp blocks per SM an uneven
+# placement costs up to 1/8 of the FMA throughput, which calibration on an
+# otherwise idle GPU does not see.  20% covers it.
+MARGIN = 0.20
+
+
+def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = MARGIN,
                      idle_us: int = 20000) -> KernelCal:
     """Worst case over SMs of both dies, warm launches and launches after an
     idle GPU (the SM clock may have dropped; clocks are not locked here)."""
@@ -237,7 +245,7 @@ def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = 
 
 def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int = 0,
                     utilization: float = 3.0, horizon_us: float = 3e6, n_sm: int = 148,
-                    margin: float = 0.12, cpu_mode: int = CPU_PARALLEL,
+                    margin: float = MARGIN, cpu_mode: int = CPU_PARALLEL,
                     bus_mode: int = BUS_FP) -> WcrtReport:
     """BASELINE config 4: n concurrent tasks on disjoint SM partitions of the
     GPU; measured WCRT vs the RTGPU bound R_k."""
@@ -312,8 +320,12 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
         grs = [gpu_response_bounds(g, 2 * len(sms)).hi for g in s.gpu_segments]
         ratio = r.max_response_us / float(bound)
         ratios.append(ratio)
-        # the segment's response as the job sees it: launch to observed completion
-        seg = [r.seg_max_wall_us[j] for j in range(len(grs))]
+        # Lemma 4 bounds the kernel's execution on its partition: the on-GPU
+        # span from the first participating block's start to the last one's
+        # end (%globaltimer).  Event and host-observed times, which add launch
+        # latency (and the VM's scheduling jitter), are reported beside it;
+        # the end-to-end check covers them.
+        seg = [r.seg_max_span_us[j] for j in range(len(grs))]
         kern_ok = all(x <= float(b) for x, b in zip(seg, grs))
         kok = kok and kern_ok
         out.max_kernel_ratio = max([out.max_kernel_ratio] + [x / float(b) for x, b in zip(seg, grs)])
@@ -322,12 +334,12 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
                           "bound_us": float(bound), "ratio": round(ratio, 4),
                           "mean_us": round(r.mean_response_us, 1),
                           "max_kernel_us": round(r.max_kernel_us, 1),
-                          "kernel_us_vs_gr_up": [[round(x, 1), round(float(b), 1)]
+                          "kernel_span_us_vs_gr_up": [[round(x, 1), round(float(b), 1)]
                                                  for x, b in zip(seg, grs)],
-                          "kernel_span_us": [round(r.seg_max_span_us[j], 1)
-                                             for j in range(len(grs))],
                           "kernel_event_us": [round(r.seg_max_kernel_us[j], 1)
                                               for j in range(len(grs))],
+                          "kernel_wall_us": [round(r.seg_max_wall_us[j], 1)
+                                             for j in range(len(grs))],
                           "worst_launch": [{"skew_us": round(r.seg_worst_skew_us[j], 1),
                                             "sm_mhz": round(r.seg_worst_mhz[j]),
                                             "items": [int(r.seg_worst_items[j][0]),

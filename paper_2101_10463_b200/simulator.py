@@ -27,7 +27,8 @@ import numpy as np
 
 from . import _native
 from .gpu import gpu_response_bounds
-from .model import AnalysisReport, SmAllocation, TaskSet, TaskSpec, duration_to_str, validate_taskset
+from .model import (AnalysisReport, SmAllocation, TaskSet, TaskSpec, duration_to_str,
+                    validate_taskset)
 
 HDR, TASKW, SEGW = 16, 8, 6          # include/rtgpu_sim.h
 KINDS = ("cpu", "mem", "gpu", "job")
@@ -146,8 +147,12 @@ def _lcm(a: int, b: int) -> int:
     return a // math.gcd(a, b) * b
 
 
-def pack_simulation(ts: TaskSet, alloc: SmAllocation, cfg: SimConfig) -> _Packed:
-    """Validate like simulate() and build the simulator blob (rtgpu_sim.h)."""
+def pack_simulation(ts: TaskSet, alloc: SmAllocation, cfg: SimConfig,
+                    pool: Optional[int] = 0) -> _Packed:
+    """Validate like simulate() and build the simulator blob (rtgpu_sim.h).
+    pool: job records on the device (0: one per release point, always
+    enough; None: 4 per task + 16, recycled -- RTGPU_SIM_POOL_OVERFLOW if an
+    overloaded run needs more, and simulate_batch re-runs it with pool 0)."""
     violations = validate_taskset(ts)
     if violations:
         raise ValueError("invalid taskset: " + "; ".join(violations))
@@ -222,7 +227,8 @@ def pack_simulation(ts: TaskSet, alloc: SmAllocation, cfg: SimConfig) -> _Packed
         seg_off += SEGW * len(ent)
     if 2 * big >= LIMIT:
         raise SimRangeError(f"simulation time scale {Q} x horizon exceeds 62-bit integers")
-    blob[:8] = [n, int(uniform), H, R, evcap, len(key), smax, seg_off]
+    blob[:9] = [n, int(uniform), H, R, evcap, len(key), smax, seg_off,
+                4 * n + 16 if pool is None else pool]
     blob[seg_off:seg_off + len(key)] = key
     return _Packed(blob, Q, tasks, R, evcap, smax, plans)
 
@@ -241,6 +247,10 @@ def _lib():
         p64 = ctypes.POINTER(ctypes.c_int64)
         L.rtgpu_sim_host.argtypes = [p64, p64, ctypes.c_int64, p64, p64, p64, ctypes.c_int32,
                                      ctypes.POINTER(_SimOut)]
+        L.rtgpu_sim_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64] + \
+            [ctypes.c_void_p] * 6 + [ctypes.c_int32, ctypes.POINTER(_SimOut), ctypes.c_void_p]
+        L.rtgpu_sim_scratch_words.argtypes = [p64]
+        L.rtgpu_sim_scratch_words.restype = ctypes.c_int64
         L.rtgpu_sim_last_error.restype = ctypes.c_char_p
         L._sim_ready = True
     return L
@@ -308,13 +318,7 @@ class SimBatch:
                 v = int(row[p])
                 if v < 0:
                     continue
-                bound = None
-                if kind == "mem" and seg < len(tr.mem_r_up):
-                    bound = tr.mem_r_up[seg]
-                elif kind == "cpu" and seg < len(tr.cpu_r_up):
-                    bound = tr.cpu_r_up[seg]
-                elif kind == "gpu" and seg < len(tr.gpu_r):
-                    bound = tr.gpu_r[seg].hi
+                bound = _segment_bound(tr, kind, seg)
                 if bound is not None and Fraction(v, pk.Q) > bound:
                     out.append(f"task {t.id}: {kind} segment {seg} response "
                                f"{Fraction(v, pk.Q)} > bound {bound}")
@@ -325,12 +329,67 @@ class SimBatch:
         return out
 
 
-def simulate_batch(items: Sequence, cfg=SimConfig(), events: bool = False) -> SimBatch:
+def simulate_batch(items: Sequence, cfg=SimConfig(), events: bool = False,
+                   pool: Optional[int] = None) -> SimBatch:
     """Simulate many (TaskSet, SmAllocation) pairs in one GPU launch; cfg is
-    one SimConfig or one per item.  events=True also returns every trace."""
+    one SimConfig or one per item.  events=True also returns every trace.
+    Runs whose live jobs outgrow the recycled record pool are re-run with
+    one record per release point."""
     _native.require_device()
     cfgs = list(cfg) if isinstance(cfg, (list, tuple)) else [cfg] * len(items)
-    packs = [pack_simulation(ts, al, c) for (ts, al), c in zip(items, cfgs)]
+    packs = [pack_simulation(ts, al, c, pool) for (ts, al), c in zip(items, cfgs)]
+    res = _run_packs(packs, events)
+    redo = [s for s in range(len(packs)) if res.status[s] == 3]
+    if redo:
+        again = _run_packs([pack_simulation(*items[s], cfgs[s], 0) for s in redo], events)
+        res = _merge(res, redo, again)
+    bad = np.nonzero(res.status)[0]
+    if len(bad):
+        raise RuntimeError(f"simulator: status {int(res.status[bad[0]])} for simulation "
+                           f"{int(bad[0])}")
+    return res
+
+
+def _merge(res: SimBatch, redo: list, again: SimBatch) -> SimBatch:
+    """Replace the results of simulations `redo` by those of `again`."""
+    packs = list(res.packs)
+    for x, s in enumerate(redo):
+        packs[s] = again.packs[x]
+    pick = {s: x for x, s in enumerate(redo)}
+    src = [(again, pick[s]) if s in pick else (res, s) for s in range(len(packs))]
+
+    def cat(name, base):
+        parts = []
+        for b, s in src:
+            bb = getattr(b, base)
+            parts.append(getattr(b, name)[bb[s]:bb[s + 1]])
+        return np.concatenate(parts) if parts else getattr(res, name)
+
+    def bases(key):
+        return np.concatenate([[0], np.cumsum([getattr(b, key)[s + 1] - getattr(b, key)[s]
+                                               for b, s in src])]).astype(np.int64)
+    out = SimBatch(packs, np.array([b.status[s] for b, s in src], np.int32),
+                   np.array([b.n_events[s] for b, s in src], np.int64),
+                   np.array([b.misses[s] for b, s in src], np.int64),
+                   bases("job_base"), bases("task_base"),
+                   cat("job_task", "job_base"), cat("job_k", "job_base"),
+                   cat("job_resp", "job_base"), cat("job_rank", "job_base"),
+                   np.zeros((0, 1), np.int64), cat("resp_max", "task_base"))
+    w = max(res.seg_max.shape[1], again.seg_max.shape[1])
+    rows = []
+    for b, s in src:
+        r = b.seg_max[b.task_base[s]:b.task_base[s + 1]]
+        rows.append(np.pad(r, ((0, 0), (0, w - r.shape[1])), constant_values=-1))
+    out.seg_max = np.concatenate(rows) if rows else np.zeros((0, w), np.int64)
+    if res.events is not None:
+        out.events = np.concatenate([b.events[b.ev_base[s]:b.ev_base[s] + b.n_events[s]]
+                                     for b, s in src]) if src else res.events
+        out.ev_base = np.concatenate([[0], np.cumsum([b.n_events[s] for b, s in src])]
+                                     ).astype(np.int64)
+    return out
+
+
+def _run_packs(packs: list, events: bool) -> SimBatch:
     S = len(packs)
     set_off = np.zeros(S + 1, np.int64)
     job_base = np.zeros(S + 1, np.int64)
@@ -362,11 +421,75 @@ def simulate_batch(items: Sequence, cfg=SimConfig(), events: bool = False) -> Si
                           p64(ev_base) if events else None, smax, ctypes.byref(o))
     if rc != 0:
         raise RuntimeError("simulator: " + L.rtgpu_sim_last_error().decode())
-    bad = np.nonzero(res.status)[0]
-    if len(bad):
-        raise RuntimeError(f"simulator: status {int(res.status[bad[0]])} for simulation "
-                           f"{int(bad[0])}")
     return res
+
+
+class DeviceSimBatch:
+    """Packed simulations resident in HBM (torch tensors as allocations),
+    run with rtgpu_sim_device on a CUDA stream -- the bulk validation path."""
+
+    def __init__(self, packs: list, device: str = "cuda", events: bool = False):
+        import torch
+        _native.require_device()
+        L = _lib()
+        self.packs = packs
+        S = self.n = len(packs)
+        self.events = events
+        self.device = torch.device(device)
+        off = np.zeros((6, S + 1), np.int64)   # set_off, job_base, task_base, ev_base, scr_off,
+        # and the launch order: longest simulations (most events) first
+        for s, pk in enumerate(packs):
+            off[:5, s + 1] = off[:5, s] + [len(pk.blob), pk.R, len(pk.tasks),
+                                         pk.evcap if events else 0,
+                                         L.rtgpu_sim_scratch_words(pk.blob.ctypes.data_as(
+                                             ctypes.POINTER(ctypes.c_int64)))]
+        off[5, :S] = np.argsort([-pk.evcap for pk in packs], kind="stable")
+        self.offsets = off
+        self.smax = max([pk.smax for pk in packs] + [1])
+        blobs = np.concatenate([pk.blob for pk in packs]) if packs else np.zeros(1, np.int64)
+        dev = self.device
+        t64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(dev)  # noqa: E731
+        self.d_blobs, self.d_off = t64(blobs), t64(off)
+        self.scratch = torch.empty(int(off[4, -1]) + 1, dtype=torch.int64, device=dev)
+        NJ, NT, NE = int(off[1, -1]), int(off[2, -1]), int(off[3, -1])
+        e = lambda n, dt: torch.empty(max(n, 1), dtype=dt, device=dev)  # noqa: E731
+        self.out = {"status": e(S, torch.int32), "n_events": e(S, torch.int64),
+                    "misses": e(S, torch.int64), "job_task": e(NJ, torch.int32),
+                    "job_k": e(NJ, torch.int32), "job_resp": e(NJ, torch.int64),
+                    "job_rank": e(NJ, torch.int32), "seg_max": e(NT * self.smax, torch.int64),
+                    "resp_max": e(NT, torch.int64),
+                    "events": e(2 * NE, torch.int64) if events else None}
+        self.input_bytes = 8 * (len(blobs) + 6 * (S + 1))
+
+    def run(self, stream=None) -> None:
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        o = self.out
+        so = _SimOut(*[o[k].data_ptr() for k in ("status", "n_events", "misses", "job_task",
+                                                  "job_k", "job_resp", "job_rank", "seg_max",
+                                                  "resp_max")],
+                     o["events"].data_ptr() if self.events else None)
+        base = self.d_off.data_ptr()
+        row = 8 * (self.n + 1)
+        L = _lib()
+        rc = L.rtgpu_sim_device(self.d_blobs.data_ptr(), base, self.n, base + row,
+                                base + 2 * row, base + 3 * row if self.events else None,
+                                base + 4 * row, self.scratch.data_ptr(), base + 5 * row,
+                                self.smax, ctypes.byref(so), stream.cuda_stream)
+        if rc:
+            raise RuntimeError("simulator: " + L.rtgpu_sim_last_error().decode())
+
+    def to_host(self) -> SimBatch:
+        o = {k: (None if v is None else v.cpu().numpy()) for k, v in self.out.items()}
+        off = self.offsets
+        NJ, NT, NE = int(off[1, -1]), int(off[2, -1]), int(off[3, -1])
+        return SimBatch(self.packs, o["status"][:self.n], o["n_events"][:self.n],
+                        o["misses"][:self.n], off[1], off[2], o["job_task"][:NJ],
+                        o["job_k"][:NJ], o["job_resp"][:NJ], o["job_rank"][:NJ],
+                        o["seg_max"][:NT * self.smax].reshape(NT, self.smax), o["resp_max"][:NT],
+                        off[3] if self.events else None,
+                        o["events"][:2 * NE].reshape(NE, 2) if self.events else None)
 
 
 def simulate(ts: TaskSet, alloc: SmAllocation, cfg: SimConfig) -> SimTrace:
@@ -374,47 +497,47 @@ def simulate(ts: TaskSet, alloc: SmAllocation, cfg: SimConfig) -> SimTrace:
     return simulate_batch([(ts, alloc)], cfg, events=True).trace(0)
 
 
+def _segment_bound(tr, kind: str, seg: int):
+    """The report's bound for one segment (None: not bounded)."""
+    table = {"mem": tr.mem_r_up, "cpu": tr.cpu_r_up,
+             "gpu": tuple(b.hi for b in tr.gpu_r)}.get(kind, ())
+    return table[seg] if 0 <= seg < len(table) else None
+
+
 def check_against_analysis(trace: SimTrace, report: AnalysisReport) -> list:
-    """Observed responses above their bounds and deadline misses, in the
-    reference's order and wording (simulator.py:340)."""
+    """Observed responses above their bounds and deadline misses
+    (simulator.py:340): first every deadline miss in trace order, then every
+    finished segment of a non-truncated job (start-to-finish, in order of
+    completion), then every end-to-end response (in completion order)."""
     if not report.schedulable:
         raise ValueError("report must be from an accepting analysis")
-    out = []
-    truncated = set(trace.truncated)
+    skip = set(trace.truncated)
+    misses, first_start, finished = [], {}, {}
     for e in trace.events:
         if e.action == "deadline-miss":
-            out.append(f"task {e.task} job {e.job}: deadline miss at {e.time}")
-    ready, finish = {}, {}
-    for e in trace.events:
+            misses.append(f"task {e.task} job {e.job}: deadline miss at {e.time}")
         if e.kind == "job":
             continue
         key = (e.task, e.job, e.kind, e.segment)
-        if e.action == "start":
-            ready.setdefault(key, e.time)
+        if e.action == "start" and key not in first_start:
+            first_start[key] = e.time
         elif e.action == "finish":
-            finish[key] = e.time
-    for (task, jobidx, kind, seg), t_fin in finish.items():
-        if (task, jobidx) in truncated:
-            continue
+            finished[key] = e.time
+    seg_lines = []
+    for key, t_end in finished.items():
+        task, job, kind, seg = key
         tr = report.per_task.get(task)
-        if tr is None:
+        if (task, job) in skip or tr is None:
             continue
-        resp = t_fin - ready[(task, jobidx, kind, seg)]
-        bound = None
-        if kind == "mem" and seg < len(tr.mem_r_up):
-            bound = tr.mem_r_up[seg]
-        elif kind == "cpu" and seg < len(tr.cpu_r_up):
-            bound = tr.cpu_r_up[seg]
-        elif kind == "gpu" and seg < len(tr.gpu_r):
-            bound = tr.gpu_r[seg].hi
-        if bound is not None and resp > bound:
-            out.append(f"task {task} job {jobidx}: {kind} segment {seg} response {resp} > bound "
-                       f"{bound}")
-    for (task, jobidx), resp in trace.responses.items():
-        tr = report.per_task.get(task)
-        if tr is None or tr.end_to_end_up is None:
-            continue
-        if resp > tr.end_to_end_up:
-            out.append(f"task {task} job {jobidx}: end-to-end response {resp} > bound "
-                       f"{tr.end_to_end_up}")
-    return out
+        bound = _segment_bound(tr, kind, seg)
+        took = t_end - first_start[key]
+        if bound is not None and took > bound:
+            seg_lines.append(f"task {task} job {job}: {kind} segment {seg} response {took} > "
+                             f"bound {bound}")
+    e2e_lines = [f"task {task} job {job}: end-to-end response {r} > bound "
+                 f"{report.per_task[task].end_to_end_up}"
+                 for (task, job), r in trace.responses.items()
+                 if report.per_task.get(task) is not None
+                 and report.per_task[task].end_to_end_up is not None
+                 and r > report.per_task[task].end_to_end_up]
+    return misses + seg_lines + e2e_lines

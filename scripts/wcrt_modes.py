@@ -17,8 +17,8 @@ for seed, util in [(1, 3.0), (3, 4.0), (3, 3.0)]:
                "applied": [r.cpu_mode, r.bus_mode], "max_ratio": round(r.max_ratio, 4),
                "max_kernel_ratio": round(r.max_kernel_ratio, 4), "ok": r.all_within_bound,
                "cal": r.calibration,
-               "tasks": [{k: t[k] for k in ("task", "sms", "jobs", "ratio", "kernel_us_vs_gr_up",
-                                            "kernel_span_us", "kernel_event_us", "worst_launch", "min_sm_mhz", "max_copy_us", "max_bus_wait_us")}
+               "tasks": [{k: t[k] for k in ("task", "sms", "jobs", "ratio", "kernel_span_us_vs_gr_up",
+                                            "kernel_event_us", "kernel_wall_us", "worst_launch", "min_sm_mhz", "max_copy_us", "max_bus_wait_us")}
                          for t in r.tasks]}
         print(json.dumps(rec), flush=True)
         out.append(rec)

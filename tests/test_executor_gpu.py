@@ -26,15 +26,13 @@ def test_kernel_time_scales_with_partition():
 
 @pytest.mark.parametrize("seed,util", [(1, 3.0), (3, 4.0)])
 def test_measured_wcrt_within_bound(seed, util):
-    """Every job's measured response stays within the analysis bound R_k.
-    Kernel times are also checked against their Lemma-4 bound; concurrent
-    partitions share the launch path and L2, so a few percent over the
-    isolated-SM model is tolerated there (and reported by bench.py)."""
+    """Every job's measured response stays within the analysis bound R_k,
+    and every kernel's on-GPU span within its Lemma-4 bound GR_up."""
     from paper_2101_10463_b200 import executor as ex
     rep = ex.wcrt_experiment(n_tasks=4, m=3, horizon_us=1.5e6, seed=seed, utilization=util)
     assert rep.schedulable, rep.note
-    detail = [(t["task"], t["ratio"], t["kernel_us_vs_gr_up"]) for t in rep.tasks]
+    detail = [(t["task"], t["ratio"], t["kernel_span_us_vs_gr_up"]) for t in rep.tasks]
     assert rep.all_within_bound, detail
-    assert rep.max_kernel_ratio <= 1.10, detail
+    assert rep.max_kernel_ratio <= 1.0, detail
     assert all(t["jobs"] > 0 for t in rep.tasks)
     assert sum(rep.allocation.values()) // 2 <= 148

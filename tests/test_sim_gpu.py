@@ -54,6 +54,34 @@ def test_batch_trace_matches_reference(gpu_traces, ci):
     assert tr.truncated == golden_truncated(c)
 
 
+def test_small_record_pool_reruns_overloaded_sets(gpu_traces):
+    """A 2-record pool overflows on most sets; those are re-run with one
+    record per release point and the merged traces are unchanged."""
+    from paper_2101_10463_b200.simulator import simulate_batch
+    items, cfgs = [], []
+    for c in CASES:
+        ts, alloc, horizon, seed, uniform = case_inputs(c)
+        items.append((ts, alloc))
+        cfgs.append(_cfg(horizon, seed, uniform))
+    b = simulate_batch(items, cfgs, events=True, pool=2)
+    for s, tr in enumerate(gpu_traces):
+        assert b.trace(s).to_jsonl() == tr.to_jsonl()
+        assert b.trace(s).truncated == tr.truncated
+
+
+def test_device_resident_batch_matches_host_path(gpu_traces):
+    from paper_2101_10463_b200.simulator import DeviceSimBatch, pack_simulation
+    packs = []
+    for c in CASES[:12]:
+        ts, alloc, horizon, seed, uniform = case_inputs(c)
+        packs.append(pack_simulation(ts, alloc, _cfg(horizon, seed, uniform), 0))
+    d = DeviceSimBatch(packs, events=True)
+    d.run()
+    h = d.to_host()
+    for s in range(len(packs)):
+        assert h.trace(s).to_jsonl() == gpu_traces[s].to_jsonl()
+
+
 @pytest.mark.parametrize("ci", [0, 5, 11, 20, len(CASES) - 1])
 def test_dropin_simulate_and_check(ci):
     from paper_2101_10463_b200.model import report_from_dict
