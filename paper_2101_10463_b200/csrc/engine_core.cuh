@@ -622,6 +622,7 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
  * _max_workload summed as in mem_response / cpu_response). */
 #ifdef RT_COUNTERS
 extern long long g_cnt_interf[2], g_cnt_lfp[2], g_cnt_eval, g_cnt_views, g_cnt_rounds;
+extern long long g_cnt_flfp[8], g_cnt_fit[8], g_cnt_frounds, g_cnt_passes;
 #define RT_COUNT(x) (x)++
 #else
 #define RT_COUNT(x)
@@ -1591,13 +1592,16 @@ template <class V, class TM>
 RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kind, int lg,
                  int PM, int half, int stride, V base, V start, V bound) {
     if (base > bound) return (V)-1;
+    RT_COUNT(g_cnt_flfp[kind]);
     const i64 prio_k = tr[k].prio;
     V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
+        RT_COUNT(g_cnt_fit[kind]);
         typename TM::template Acc<V> acc;
         tm.acc_init(acc);
         if (r > 0)
             for (int i0 = 0; i0 < k; i0 += (32 >> lg)) {
+                RT_COUNT(g_cnt_frounds);
                 tm.group_max_round(lg, [&](int slot, V &w, V &rr, bool &es) {
                     int i = i0 + (slot >> lg), h = slot & ((1 << lg) - 1);
                     if (i < k) {
@@ -1718,6 +1722,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         V sum_cr = -1; /* not computed yet; -2: some CR is None */
         /* task k passes at count g?  (R2 with the MR upper bound, then exact) */
         auto passes = [&](int g) -> int {
+            RT_COUNT(g_cnt_passes);
             const V grup = t.isgpu ? (V)t.sInfl * (V)(q / (2 * A * (Qt)g)) + Num<V>::sc(t.sGL, q) : (V)0;
             const V cl = Num<V>::sc(t.sClu, q);
             if (t.p > 0 || !have_exact_mr) {

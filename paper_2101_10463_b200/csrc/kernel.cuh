@@ -168,6 +168,50 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) front_kernel(KP
         __syncwarp();
     }
 }
+
+/* Stage 0 when the fast path applies (RTGPU, verdict only): the fast path
+ * and nothing else, so neither the general path's stack frame and
+ * registers nor its code sit in this kernel -- sets it cannot decide go to
+ * stage 1's list like the front kernel's escalations. */
+__global__ void __launch_bounds__(256, MinBlocks<double>::value) fast_kernel(KParams p) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    Layout<double> L;
+    L.init(p.dims);
+    SetCtx<double> c;
+    kernel_ctx(c, p.dims, L, warp);
+    c.budget = p.budget;
+    c.method = p.method;
+    WarpTeam tm{lane};
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(p.wctr0, 1ull);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if ((i64)idx >= p.n_sets) break;
+        const i64 s = p.set_base + (i64)idx;
+        c.blob = p.blobs + p.set_off[s];
+        const i64 tb = p.task_base[s];
+        int st = fast_verdict(tm, c, p.vsm + tb);
+        if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
+        if (st == ST_ESCALATE) {
+            if (lane == 0) {
+                unsigned long long pos = atomicAdd(&p.ctr[4], 1ull);
+                p.esc[0][pos] = s;
+            }
+            __syncwarp();
+            continue;
+        }
+        if (st != RTGPU_SCHEDULABLE) {
+            const int n = (int)c.blob[0];
+            for (int i = lane; i < n; i += 32) p.vsm[tb + i] = 0; /* no allocation */
+        }
+        if (lane == 0) {
+            p.status[s] = st;
+            p.evals[s] = c.evals;
+        }
+        __syncwarp();
+    }
+}
 #endif
 
 /* ------------------------------------------------------------ point queries */
@@ -308,6 +352,9 @@ inline int launch_front(const KParams &p, cudaStream_t st) {
         set_err_msg("task sets too large for shared memory");
         return -3;
     }
+    if (p.use_fast && !(p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128)))
+        return launch_persistent((void *)fast_kernel, p.dims, 0, (p.n_sets + wpb - 1) / wpb, wpb, bytes,
+                                 st, "fast_kernel launch", p, 0, true);
     return launch_persistent((void *)front_kernel, p.dims, 0, (p.n_sets + wpb - 1) / wpb, wpb, bytes,
                              st, "front_kernel launch", p, 0, true);
 }
