@@ -183,6 +183,29 @@ template <class T> RT_HD T lcm_lim(T a, T b, T lim) {
     return a1 * b;
 }
 
+/* lcm(1..n) for n <= 42 (lcm(1..43) exceeds int64): the fast path's
+ * scale factor, a constant per GN instead of GN - 1 gcd loops per set */
+#define RT_LCM_TABLE                                                                                      \
+    {1LL, 1LL, 2LL, 6LL, 12LL, 60LL, 60LL, 420LL, 840LL, 2520LL, 2520LL, 27720LL, 27720LL, 360360LL,            \
+     360360LL, 360360LL, 720720LL, 12252240LL, 12252240LL, 232792560LL, 232792560LL, 232792560LL,           \
+     232792560LL, 5354228880LL, 5354228880LL, 26771144400LL, 26771144400LL, 80313433200LL,                  \
+     80313433200LL, 2329089562800LL, 2329089562800LL, 72201776446800LL, 144403552893600LL,                  \
+     144403552893600LL, 144403552893600LL, 144403552893600LL, 144403552893600LL, 5342931457063200LL,        \
+     5342931457063200LL, 5342931457063200LL, 5342931457063200LL, 219060189739591200LL,                      \
+     219060189739591200LL}
+#ifdef __CUDACC__
+static __constant__ i64 rt_lcm_dev[43] = RT_LCM_TABLE;
+#endif
+static const i64 rt_lcm_host[43] = RT_LCM_TABLE;
+RT_HD i64 lcm_upto(int n) {
+    if (n < 0 || n > 42) return 0;
+#ifdef __CUDA_ARCH__
+    return rt_lcm_dev[n];
+#else
+    return rt_lcm_host[n];
+#endif
+}
+
 /* ------------------------------------------------------------ segment access */
 
 /* A task's segment area in either blob format: int64 words (header word 7
@@ -200,6 +223,15 @@ struct SegPtr {
         r.w = w;
         return r;
     }
+};
+
+/* The compact (int32) segment area with the width known at compile time:
+ * the verdict fast path runs only on compact blobs, so its reads are plain
+ * 32-bit loads with no per-access width select. */
+struct Seg32 {
+    const int32_t *p;
+    RT_HD i64 operator[](int j) const { return p[j]; }
+    RT_HD Seg32 operator+(int j) const { return Seg32{p + j}; }
 };
 
 /* ------------------------------------------------------------ per-task data */
@@ -445,14 +477,19 @@ struct SeqTeam {
 /* Build the CPU and (if any) memory chain views of task i at scale q.
  * Gap definitions: analysis.py:89 cpu_inter_arrival, analysis.py:57
  * mem_inter_arrival; GR lo from gpu.py:25 gpu_response_bounds. */
-template <class V>
+template <class V> RT_HD SegPtr seg_area(const SetCtx<V> &c, i64 off, SegPtr *) { return c.segs(off); }
+template <class V> RT_HD Seg32 seg_area(const SetCtx<V> &c, i64 off, Seg32 *) {
+    return Seg32{(const int32_t *)c.blob + off};
+}
+
+template <class V, class SA = SegPtr>
 RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     typedef Num<V> N;
     const TaskRec &t = c.TR()[i];
-    const SegPtr sg = c.segs(t.seg);
+    const SA sg = seg_area(c, t.seg, (SA *)nullptr);
     const int m = t.m, p = t.p, g = m - 1;
-    const SegPtr cl_lo = sg, cl_hi = sg + m, ml_lo = sg + 2 * m, ml_hi = ml_lo + p;
-    const SegPtr gw_lo = ml_hi + p;
+    const SA cl_lo = sg, cl_hi = sg + m, ml_lo = sg + 2 * m, ml_hi = ml_lo + p;
+    const SA gw_lo = ml_hi + p;
     typename Num<V>::Qt perlo = t.isgpu ? q / (2 * (typename Num<V>::Qt)t.g) : q;
     if (c.single_seg) {
         /* busy-waiting baseline (analysis.py:360): one execution segment of
@@ -1513,17 +1550,17 @@ RT_NI void load_task_fast(SetCtx<V> &c, int i) {
         t.B = 0;
         return;
     }
-    const SegPtr sg = c.segs(t.seg);
+    const Seg32 sg{(const int32_t *)c.blob + t.seg}; /* compact blob (checked by the caller) */
     i64 clu = 0, cll = 0, mlu = 0, mll = 0, gwl = 0, infl = 0, gls = 0, inner = 0, mx = 0, ih = 0;
-    bool bad = false;
-    for (int j = 0; j < 2 * m + 2 * p + 4 * g; j++) {
-        const i64 v = sg[j];
-        bad = bad || v < 0 || v >= ((i64)1 << 31);
-    }
-    if (bad) {
-        t.flags = TF_UNSUP;
-        t.B = 0;
-        return;
+    {
+        /* every value must be non-negative: one OR per value, then the sign */
+        int32_t acc = 0;
+        for (int j = 0; j < 2 * m + 2 * p + 4 * g; j++) acc |= sg.p[j];
+        if (acc < 0) {
+            t.flags = TF_UNSUP;
+            t.B = 0;
+            return;
+        }
     }
     for (int j = 0; j < m; j++) {
         clu += sg[m + j];
@@ -1639,7 +1676,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     c.mm = (int)h[2];
     c.A = A;
     c.segw = (int)h[7];
-    if (c.segw < 0 || c.segw > 1) return ST_ESCALATE;
+    if (c.segw != 1) return ST_ESCALATE; /* the fast path reads compact blobs only */
     c.single_seg = 0;
     c.vn = 0;
     c.vq = 0;
@@ -1664,12 +1701,8 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     const i128 vb = (i128)vb_max * range_factor(n, c.MC, c.MP);
     if (vb > (i128)Num<V>::limit()) return ST_ESCALATE_RANGE;
     const Qt qlim = Num<V>::limit() / (Qt)vb;
-    Qt L = 1;
-    for (int g = 2; g <= GN; g++) {
-        L = lcm_lim<Qt>(L, (Qt)g, qlim);
-        if (L == 0) return ST_ESCALATE_RANGE;
-    }
-    if (L > qlim / (2 * A)) return ST_ESCALATE_RANGE;
+    const Qt L = lcm_upto(GN);
+    if (L == 0 || (i128)L * (2 * A) > (i128)qlim) return ST_ESCALATE_RANGE;
     const Qt q = L * 2 * A;
     c.Vb = (i64)vb;
     c.qlim = qlim;
@@ -1688,13 +1721,18 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     V *bases = c.SCR();
     V *outs = c.SCR() + (c.MP + c.MC + 2);
     int *ord = (int *)(c.SCR() + c.L.scr_n) - 32;
+    /* L / g for every count g (GR up = sInfl * L/g + GL at scale q): one
+     * lane-parallel division per set instead of a 64-bit division per
+     * evaluation; outs has room when GN <= scr_n - (MP + MC + 2) - 32 */
+    const bool lg_tab = GN <= c.L.scr_n - (c.MP + c.MC + 2) - 32;
+    if (lg_tab) tm.pfor(GN, [&](int x) { outs[x] = (V)(L / (Qt)(x + 1)); });
     i64 used = 0, rest_min = need;
     for (int k = 0; k < n; k++) {
         const TaskRec &t = tr[k];
         /* views of tasks before k (their counts are final) */
-        if (k > 0) tm.pfor(1, [&](int) { build_view(c, k - 1, q); });
-        const SegPtr sg = c.segs(t.seg);
-        const SegPtr cl_hi = sg + t.m, ml_hi = sg + 2 * t.m + t.p;
+        if (k > 0) tm.pfor(1, [&](int) { build_view<V, Seg32>(c, k - 1, q); });
+        const Seg32 sg{(const int32_t *)c.blob + t.seg};
+        const Seg32 cl_hi = sg + t.m, ml_hi = sg + 2 * t.m + t.p;
         const V D = Num<V>::sc(t.D, q);
         int glo = 0, ghi = 0;
         if (t.isgpu) {
@@ -1723,7 +1761,9 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         /* task k passes at count g?  (R2 with the MR upper bound, then exact) */
         auto passes = [&](int g) -> int {
             RT_COUNT(g_cnt_passes);
-            const V grup = t.isgpu ? (V)t.sInfl * (V)(q / (2 * A * (Qt)g)) + Num<V>::sc(t.sGL, q) : (V)0;
+            const V grup = t.isgpu ? (V)t.sInfl * (lg_tab ? outs[g - 1] : (V)(q / (2 * A * (Qt)g))) +
+                                         Num<V>::sc(t.sGL, q)
+                                   : (V)0;
             const V cl = Num<V>::sc(t.sClu, q);
             if (t.p > 0 || !have_exact_mr) {
                 const V b2 = grup + mr_ub + cl;
@@ -1792,7 +1832,6 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
             if (sum_cr < 0) return 0;
             return grup + sum_mr + sum_cr <= D ? 1 : 0;
         };
-        (void)outs;
         c.evals++;
         /* smallest passing count: glo, else ghi, else bisection -- one call
          * site for `passes` keeps a single inlined copy */

@@ -78,14 +78,20 @@ def test_engine_core_matches_oracle_generated(n, m, gn, u, mm, mi):
                                          (8, 5, 10, "3/5", 1), (5, 3, 10, "1", 0),
                                          (6, 2, 20, "4/5", 0), (16, 9, 10, "1/5", 0)])
 def test_verdict_fast_path_matches_oracle(n, m, gn, u, mm):
-    """Verdict-only runs take the front stage's fast path (flags = 0)."""
-    gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), Fraction(u), mm,
-                              gn, Fraction(12, 100), Fraction(1) if mm == 0 else Fraction(7, 10))
-    b, so, tb = _native.generate(gp, [f"3:{u}:{i}" for i in range(200)])
-    o = oracle.analyze_batch(b, so, tb, flags=0, threads=8, detail=False)
-    h = harness.analyze_batch(b, so, tb, flags=0, detail=False)
-    if gn <= 12:  # the fast path needs 2*A*lcm(1..GN) to fit FP64 exactly
-        assert (h["stage"] == -1).mean() > 0.5
-    assert np.array_equal(o["status"], h["status"])
-    sched = np.repeat(o["status"] == 1, n)
-    assert np.array_equal(o["vsm"][sched], h["vsm"][sched])
+    """Verdict-only runs on compact (int32) blobs take the fast path
+    (flags = 0); int64 blobs of the same sets go to the general path and
+    give the same verdicts."""
+    for compact in (True, False):
+        gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), Fraction(u),
+                                  mm, gn, Fraction(12, 100),
+                                  Fraction(1) if mm == 0 else Fraction(7, 10), compact=compact)
+        b, so, tb = _native.generate(gp, [f"3:{u}:{i}" for i in range(200)])
+        o = oracle.analyze_batch(b, so, tb, flags=0, threads=8, detail=False)
+        h = harness.analyze_batch(b, so, tb, flags=0, detail=False)
+        if compact and gn <= 12:  # the fast path needs 2*A*lcm(1..GN) to fit FP64 exactly
+            assert (h["stage"] == -1).mean() > 0.5
+        if not compact:
+            assert (h["stage"] >= 0).all()
+        assert np.array_equal(o["status"], h["status"])
+        sched = np.repeat(o["status"] == 1, n)
+        assert np.array_equal(o["vsm"][sched], h["vsm"][sched])
