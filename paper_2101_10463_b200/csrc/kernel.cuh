@@ -40,6 +40,14 @@ struct KParams {
     unsigned long long *wctr0; /* front stage: this launch's work counter */
 };
 
+/* fast kernel: second chance for range escalations in an int64 instance
+ * of the fast path.  Measured slower (stage 0 4.79 -> 6.77 ms per 100 000
+ * sets: the second instance costs the FP64 path registers and spills) even
+ * though it empties stage 1 (0.86 -> 0.37 ms).  Off. */
+#ifndef RTGPU_FAST_I64
+#define RTGPU_FAST_I64 0
+#endif
+
 /* minimum resident CTAs per SM the register allocation must allow */
 #ifndef RTGPU_MINB
 #define RTGPU_MINB 4
@@ -182,6 +190,17 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) fast_kernel(KPa
     kernel_ctx(c, p.dims, L, warp);
     c.budget = p.budget;
     c.method = p.method;
+#if RTGPU_FAST_I64
+    /* the int64 instance of the fast path shares the warp's slab (same
+     * layout: 8-byte values) and takes the sets whose fixed scale does not
+     * fit FP64's 2^52 -- in the same warp, without a separate launch */
+    Layout<i64> L64;
+    L64.init(p.dims);
+    SetCtx<i64> c64;
+    kernel_ctx(c64, p.dims, L64, warp);
+    c64.budget = p.budget;
+    c64.method = p.method;
+#endif
     WarpTeam tm{lane};
     for (;;) {
         unsigned long long idx = 0;
@@ -192,6 +211,13 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) fast_kernel(KPa
         c.blob = p.blobs + p.set_off[s];
         const i64 tb = p.task_base[s];
         int st = fast_verdict(tm, c, p.vsm + tb);
+#if RTGPU_FAST_I64
+        if (st == ST_ESCALATE_RANGE) {
+            c64.blob = c.blob;
+            st = fast_verdict(tm, c64, p.vsm + tb);
+            c.evals = c64.evals;
+        }
+#endif
         if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
         if (st == ST_ESCALATE) {
             if (lane == 0) {
@@ -335,12 +361,11 @@ template <class V> inline int launch_stage(const KParams &p, int stage, cudaStre
         set_err_msg("task sets too large for shared memory");
         return -3;
     }
-    /* the list length is only known on the device: a persistent grid of
-     * two CTAs per SM (escalations are few) */
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return launch_persistent((void *)analyze_kernel<V>, p.dims, 0, (i64)sms * 2, wpb, bytes, st,
+    /* the list length is only known on the device: a persistent grid at
+     * full occupancy (a hard set takes one warp ~0.4 ms in the general path,
+     * so the stage's time is its longest warp: spread the list over every
+     * resident warp; idle warps exit at once) */
+    return launch_persistent((void *)analyze_kernel<V>, p.dims, 0, -1, wpb, bytes, st,
                              "analyze_kernel launch", p, stage, false);
 }
 

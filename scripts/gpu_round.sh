@@ -11,3 +11,14 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-wcrt --no-sim > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu-launch rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fast_kernel|front_kernel" -s 3 -c 1 -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-wcrt --no-sim > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu-full rc=$?"
 tail -3 gpurun_out/ncu_full_$TAG.log
+python - <<'PY' > gpurun_out/h2d_$TAG.txt 2>&1
+import torch, time
+x = torch.empty(192 << 20, dtype=torch.uint8, pin_memory=True)
+y = torch.empty_like(x, device="cuda")
+for _ in range(3): y.copy_(x, non_blocking=True)
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record(); [y.copy_(x, non_blocking=True) for _ in range(10)]; e.record(); torch.cuda.synchronize()
+print("H2D GB/s", 10 * x.numel() / (s.elapsed_time(e) * 1e-3) / 1e9)
+PY
+cat gpurun_out/h2d_$TAG.txt
