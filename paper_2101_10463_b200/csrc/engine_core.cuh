@@ -518,6 +518,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         VOff o(c.MC);
         V *v = c.VC() + (size_t)i * c.L.SC;
         V P = 0, EP = 0;
+        #pragma unroll 1
         for (int j = 0; j < m; j++) {
             V e = N::sc(cl_hi[j], q);
             v[o.e + j] = e;
@@ -547,6 +548,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         VOff o(c.MP);
         V *v = c.VM() + (size_t)i * c.L.SM;
         V P = 0, EP = 0;
+        #pragma unroll 1
         for (int j = 0; j < p; j++) {
             V e = N::sc(ml_hi[j], q);
             v[o.e + j] = e;
@@ -1555,6 +1557,7 @@ RT_NI void load_task_fast(SetCtx<V> &c, int i) {
     {
         /* every value must be non-negative: one OR per value, then the sign */
         int32_t acc = 0;
+        #pragma unroll 1
         for (int j = 0; j < 2 * m + 2 * p + 4 * g; j++) acc |= sg.p[j];
         if (acc < 0) {
             t.flags = TF_UNSUP;
@@ -1562,17 +1565,20 @@ RT_NI void load_task_fast(SetCtx<V> &c, int i) {
             return;
         }
     }
+    #pragma unroll 1
     for (int j = 0; j < m; j++) {
         clu += sg[m + j];
         cll += sg[j];
         if (j >= 1 && j <= m - 2) inner += sg[j];
     }
+    #pragma unroll 1
     for (int j = 0; j < p; j++) {
         mll += sg[2 * m + j];
         const i64 h = sg[2 * m + p + j];
         mlu += h;
         mx = tmax(mx, h);
     }
+    #pragma unroll 1
     for (int j = 0; j < g; j++) {
         const i64 lo = sg[2 * m + 2 * p + j], hi = sg[2 * m + 2 * p + g + j];
         const i64 gl = sg[2 * m + 2 * p + 2 * g + j], an = sg[2 * m + 2 * p + 3 * g + j];
@@ -1687,8 +1693,10 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     TaskRec *tr = c.TR();
     tm.pfor(n, [&](int i) { load_task_fast(c, i); });
     i64 vb_max = 0, need = 0;
+    #pragma unroll 1
     for (int k = 0; k < n; k++)
         if (tr[k].flags & (TF_UNSUP | TF_IRREG)) return ST_ESCALATE;
+    #pragma unroll 1
     for (int k = 0; k < n; k++) {
         const TaskRec &t = tr[k];
         if (t.flags & TF_INV) return ST_ESCALATE;             /* the reference raises */
@@ -1711,6 +1719,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     tm.sync();
     tm.pfor(n, [&](int k) {
         i64 b = 0;
+        #pragma unroll 1
         for (int i = 0; i < n; i++)
             if (tr[i].prio > tr[k].prio) b = tmax(b, tr[i].maxMlu);
         tr[k].B = b;
@@ -1727,6 +1736,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     const bool lg_tab = GN <= c.L.scr_n - (c.MP + c.MC + 2) - 32;
     if (lg_tab) tm.pfor(GN, [&](int x) { outs[x] = (V)(L / (Qt)(x + 1)); });
     i64 used = 0, rest_min = need;
+    #pragma unroll 1
     for (int k = 0; k < n; k++) {
         const TaskRec &t = tr[k];
         /* views of tasks before k (their counts are final) */
@@ -1747,6 +1757,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         bool have_exact_mr = t.p == 0;
         if (t.p > 0) {
             i64 bmax_t = 0, bsum_t = 0;
+            #pragma unroll 1
             for (int j = 0; j < t.p; j++) {
                 bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
                 bsum_t += ml_hi[j] + t.B;
@@ -1775,11 +1786,13 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                     tm.pfor(t.p, [&](int j) { bases[j] = Num<V>::sc(ml_hi[j] + t.B, q); });
                     tm.pfor(t.p, [&](int j) {
                         int rk = 0;
+                        #pragma unroll 1
                         for (int x = 0; x < t.p; x++)
                             rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
                         ord[rk] = j;
                     });
                     V pb = 0, pr = 0, acc = 0;
+                    #pragma unroll 1
                     for (int st = 0; st < t.p; st++) {
                         const V b = bases[ord[st]];
                         const V r0 = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, b,
@@ -1809,11 +1822,13 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                 tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q); });
                 tm.pfor(t.m, [&](int j) {
                     int rk = 0;
+                    #pragma unroll 1
                     for (int x = 0; x < t.m; x++)
                         rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
                     ord[rk] = j;
                 });
                 V pb = 0, pr = 0, acc = 0;
+                #pragma unroll 1
                 for (int st = 0; st < t.m; st++) {
                     const V b = bases[ord[st]];
                     const V r0 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b,
@@ -1837,6 +1852,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
          * site for `passes` keeps a single inlined copy */
         int g = 0, lo = glo, hi = ghi, phase = t.isgpu ? 0 : 3;
         int cand = t.isgpu ? glo : 0;
+        #pragma unroll 1
         for (;;) {
             const int o = passes(cand);
             if (o < 0) return ST_ESCALATE;
