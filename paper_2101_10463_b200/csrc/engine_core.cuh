@@ -382,6 +382,8 @@ struct WarpTeam {
     __device__ __forceinline__ void sync() const { __syncwarp(); }
     __device__ __forceinline__ bool leader() const { return lane == 0; }
     template <class F> __device__ __forceinline__ void pfor(int n, F f) const {
+        /* one copy of the body: these loops are setup code (n <= 64) */
+#pragma unroll 1
         for (int i = lane; i < n; i += 32) f(i);
         __syncwarp();
     }
