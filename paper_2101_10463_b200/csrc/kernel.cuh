@@ -36,6 +36,8 @@ struct KParams {
     unsigned long long *ctr;
     i64 *esc[3];
     int use_fast;              /* front stage runs the verdict fast path */
+    int last_stage;            /* escalating past this general stage is RTGPU_RANGE (3; 2 in
+                                * verdict runs, whose general stages are int64 then int128) */
     i64 set_base;              /* front stage: first set of this launch (chunked e2e path) */
     unsigned long long *wctr0; /* front stage: this launch's work counter */
 };
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
                            (stage == 2 && (p.flags & RTGPU_F_FIRST_I128));
         int st = force ? (int)ST_ESCALATE : analyze_set(tm, c, p.flags, o);
         if (st == ST_ESCALATE) {
-            if (stage < 3) {
+            if (stage < p.last_stage) {
                 if (lane == 0) {
                     unsigned long long pos = atomicAdd(&p.ctr[4 + stage], 1ull);
                     p.esc[stage][pos] = s;

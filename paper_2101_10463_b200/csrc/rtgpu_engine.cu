@@ -86,6 +86,31 @@ int scan_dims_host(const i64 *blobs, const i64 *set_off, i64 n_sets, Dims *d) {
     return 0;
 }
 
+
+/* The general stages after stage 0.  Verdict runs (the fast path in stage
+ * 0) take stage 0's escalations -- mostly sets whose fixed FP64 scale does
+ * not fit, a few thousand per 100 000 -- straight to the int64 general path
+ * (then int128): their latency, not their number, sets the stages' time,
+ * and an FP64 general pass in between only lengthened the chain for the
+ * hardest sets.  Other runs: FP64, int64, int128. */
+int launch_general(KParams &p, cudaStream_t st) {
+    int rc = 0;
+    if (p.use_fast && !(p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) {
+        p.last_stage = 2;
+        rc = launch_stage_i64(p, 1, st);
+        if (g_timing) cudaEventRecord(g_ev[2], st);
+        if (!rc) rc = launch_stage_i128(p, 2, st);
+    } else {
+        p.last_stage = 3;
+        rc = launch_stage_f64(p, 1, st);
+        if (!rc) rc = launch_stage_i64(p, 2, st);
+        if (g_timing) cudaEventRecord(g_ev[2], st);
+        if (!rc) rc = launch_stage_i128(p, 3, st);
+    }
+    if (g_timing) cudaEventRecord(g_ev[3], st);
+    return rc;
+}
+
 int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base, i64 n_sets,
                const Dims &dims, int method, unsigned flags, i64 budget, int32_t *d_status,
                i64 *d_evals, int32_t *d_vsm, i64 *d_e2e, i64 *d_den, i64 *d_detail,
@@ -137,11 +162,7 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     if (g_timing) cudaEventRecord(g_ev[0], st);
     int rc = launch_front_f64(p, st);
     if (g_timing) cudaEventRecord(g_ev[1], st);
-    if (!rc) rc = launch_stage_f64(p, 1, st);
-    if (!rc) rc = launch_stage_i64(p, 2, st);
-    if (g_timing) cudaEventRecord(g_ev[2], st);
-    if (!rc) rc = launch_stage_i128(p, 3, st);
-    if (g_timing) cudaEventRecord(g_ev[3], st);
+    rc = rc ? rc : launch_general(p, st);
     g_ev_valid = g_timing && !rc;
     g_last_ctr = p.ctr;
     g_last_n = n_sets;
@@ -351,9 +372,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
     cudaStreamWaitEvent(g_s_comp[0], g_ev_comp[1], 0);
     cudaStream_t st = g_s_comp[0];
     p.n_sets = n_sets;
-    rc = launch_stage_f64(p, 1, st);
-    if (!rc) rc = launch_stage_i64(p, 2, st);
-    if (!rc) rc = launch_stage_i128(p, 3, st);
+    rc = launch_general(p, st);
     if (rc) return rc;
     cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, st);
