@@ -36,19 +36,17 @@ struct KParams {
     unsigned long long *ctr;
     i64 *esc[3];
     int use_fast;              /* front stage runs the verdict fast path */
-    int last_stage;            /* escalating past this general stage is RTGPU_RANGE (3; 2 in
+    int last_stage = 3;        /* escalating past this general stage is RTGPU_RANGE (3; 2 in
                                 * verdict runs, whose general stages are int64 then int128) */
+    /* streamed input (end-to-end path): set s of chunk c = the c with
+     * n*c/chunks <= s < n*(c+1)/chunks is readable once chunk_flag[c] ==
+     * epoch (the copy stream writes it after the chunk's H2D copy) */
+    const unsigned long long *chunk_flag = nullptr;
+    unsigned long long epoch = 0;
+    int chunks = 1;
     i64 set_base;              /* front stage: first set of this launch (chunked e2e path) */
     unsigned long long *wctr0; /* front stage: this launch's work counter */
 };
-
-/* fast kernel: second chance for range escalations in an int64 instance
- * of the fast path.  Measured slower (stage 0 4.79 -> 6.77 ms per 100 000
- * sets: the second instance costs the FP64 path registers and spills) even
- * though it empties stage 1 (0.86 -> 0.37 ms).  Off. */
-#ifndef RTGPU_FAST_I64
-#define RTGPU_FAST_I64 0
-#endif
 
 /* minimum resident CTAs per SM the register allocation must allow */
 #ifndef RTGPU_MINB
@@ -179,10 +177,40 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) front_kernel(KP
     }
 }
 
+/* Wait until the chunk holding set s has arrived (streamed input).  Lane 0
+ * polls the chunk's flag, backing off with nanosleep.  The first set of a
+ * chunk always takes an acquire load plus an acquire fence: a 128-byte line
+ * spanning the chunk boundary may sit in this SM's L1 from the previous
+ * chunk's last set, loaded before this chunk's bytes arrived, and the
+ * acquire invalidates it.  Lines of any other set lie wholly in its chunk and
+ * are never loaded before the chunk's flag is seen. */
+__device__ __forceinline__ void wait_chunk(const KParams &p, i64 s, int lane) {
+    if (lane == 0) {
+        const i64 n = p.n_sets, C = p.chunks;
+        i64 c = s * C / n;
+        while (c + 1 < C && n * (c + 1) / C <= s) c++;
+        while (c > 0 && n * c / C > s) c--;
+        const bool first = s == n * c / C;
+        const unsigned long long *f = p.chunk_flag + c;
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+        if (v != p.epoch || first) {
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+                if (v == p.epoch) break;
+                __nanosleep(256);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+    }
+    __syncwarp();
+}
+
 /* Stage 0 when the fast path applies (RTGPU, verdict only): the fast path
  * and nothing else, so neither the general path's stack frame and
  * registers nor its code sit in this kernel -- sets it cannot decide go to
  * stage 1's list like the front kernel's escalations. */
+template <bool STREAM>
 __global__ void __launch_bounds__(256, MinBlocks<double>::value) fast_kernel(KParams p) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -192,17 +220,6 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) fast_kernel(KPa
     kernel_ctx(c, p.dims, L, warp);
     c.budget = p.budget;
     c.method = p.method;
-#if RTGPU_FAST_I64
-    /* the int64 instance of the fast path shares the warp's slab (same
-     * layout: 8-byte values) and takes the sets whose fixed scale does not
-     * fit FP64's 2^52 -- in the same warp, without a separate launch */
-    Layout<i64> L64;
-    L64.init(p.dims);
-    SetCtx<i64> c64;
-    kernel_ctx(c64, p.dims, L64, warp);
-    c64.budget = p.budget;
-    c64.method = p.method;
-#endif
     WarpTeam tm{lane};
     for (;;) {
         unsigned long long idx = 0;
@@ -210,16 +227,24 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) fast_kernel(KPa
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if ((i64)idx >= p.n_sets) break;
         const i64 s = p.set_base + (i64)idx;
+        if (STREAM) {
+            wait_chunk(p, s, lane);
+            /* the layout was sized from a sample of the batch: a set beyond
+             * it goes to the oversize list (esc[2], unused by verdict runs)
+             * and the host re-runs it with the batch's true dims */
+            const i64 *h = p.blobs + p.set_off[s];
+            if (h[0] > p.dims.maxn || h[5] > p.dims.MC || h[6] > p.dims.MP) {
+                if (lane == 0) {
+                    unsigned long long pos = atomicAdd(&p.ctr[6], 1ull);
+                    p.esc[2][pos] = s;
+                }
+                __syncwarp();
+                continue;
+            }
+        }
         c.blob = p.blobs + p.set_off[s];
         const i64 tb = p.task_base[s];
         int st = fast_verdict(tm, c, p.vsm + tb);
-#if RTGPU_FAST_I64
-        if (st == ST_ESCALATE_RANGE) {
-            c64.blob = c.blob;
-            st = fast_verdict(tm, c64, p.vsm + tb);
-            c.evals = c64.evals;
-        }
-#endif
         if (st == ST_ESCALATE_RANGE) st = ST_ESCALATE;
         if (st == ST_ESCALATE) {
             if (lane == 0) {
@@ -380,8 +405,8 @@ inline int launch_front(const KParams &p, cudaStream_t st) {
         return -3;
     }
     if (p.use_fast && !(p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128)))
-        return launch_persistent((void *)fast_kernel, p.dims, 0, (p.n_sets + wpb - 1) / wpb, wpb, bytes,
-                                 st, "fast_kernel launch", p, 0, true);
+        return launch_persistent(p.chunk_flag ? (void *)fast_kernel<true> : (void *)fast_kernel<false>, p.dims,
+                                 0, (p.n_sets + wpb - 1) / wpb, wpb, bytes, st, "fast_kernel launch", p, 0, true);
     return launch_persistent((void *)front_kernel, p.dims, 0, (p.n_sets + wpb - 1) / wpb, wpb, bytes,
                              st, "front_kernel launch", p, 0, true);
 }
