@@ -859,6 +859,7 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
          * passes with the resulting upper bound on sum MR it passes exactly
          * (the least fixed point is monotone in the base). */
         i64 bmax_t = 0, bsum_t = 0;
+        #pragma unroll 1
         for (int j = 0; j < t.p; j++) {
             bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
             bsum_t += ml_hi[j] + t.B;
@@ -878,6 +879,7 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
     if (t.p > 0) {
         tm.pfor(t.p, [&](int j) { bases[j] = N::sc(ml_hi[j] + t.B, q); });
         lfp_many(tm, c, k, K_MEM, bases, outs, t.p, D, !want_all, mr_none);
+        #pragma unroll 1
         for (int j = 0; j < t.p; j++)
             if (outs[j] >= 0) sum_mr += outs[j];
         if (mr_out) tm.pfor(t.p, [&](int j) { mr_out[j] = outs[j]; });
@@ -899,6 +901,7 @@ RT_NI void eval_task(const TM &tm, SetCtx<V> &c, int k, int g, typename Num<V>::
     bool cr_none;
     lfp_many(tm, c, k, K_CPU, bases, outs, t.m, D, !want_all, cr_none);
     V sum_cr = 0;
+    #pragma unroll 1
     for (int j = 0; j < t.m; j++)
         if (outs[j] >= 0) sum_cr += outs[j];
     if (cr_out) tm.pfor(t.m, [&](int j) { cr_out[j] = outs[j]; });
@@ -950,12 +953,14 @@ RT_NI void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
     i128 tot = 0;
     t.sClu = t.sCll = t.sMlu = t.sMll = t.sGWlo = t.sInfl = t.sGL = t.innerCll = t.maxMlu = 0;
     bool neg = false;
+    #pragma unroll 1
     for (int j = 0; j < m; j++) {
         t.sClu += cl_hi[j];
         t.sCll += cl_lo[j];
         neg = neg || cl_hi[j] < 0 || cl_lo[j] < 0;
         if (j >= 1 && j <= m - 2) t.innerCll += cl_lo[j];
     }
+    #pragma unroll 1
     for (int j = 0; j < p; j++) {
         t.sMlu += ml_hi[j];
         t.sMll += ml_lo[j];
@@ -963,6 +968,7 @@ RT_NI void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
         neg = neg || ml_hi[j] < 0 || ml_lo[j] < 0;
     }
     i128 infl_hi = 0;
+    #pragma unroll 1
     for (int j = 0; j < g; j++) {
         neg = neg || gw_lo[j] < 0 || gw_hi[j] < 0 || gl[j] < 0 || an[j] < 0;
         i128 w = (i128)gw_hi[j] * an[j], o = (i128)gl[j] * c.A;
@@ -1030,6 +1036,7 @@ RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool sto
     V *grh = grl + c.MC;
     bool failed = false;
     int k = 0;
+    #pragma unroll 1
     for (; k < c.n; k++) {
         const TaskRec &t = c.TR()[k];
         TaskEval<V> res;
@@ -1054,10 +1061,13 @@ RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool sto
         if (sizeof(V) > 8) {
             i128 gg = (i128)q;
             if (res.e2e >= 0) gg = gcdq<i128>(gg, Num<V>::wide(res.e2e));
+            #pragma unroll 1
             for (int j = 0; j < p; j++)
                 if (mr[j] >= 0) gg = gcdq<i128>(gg, Num<V>::wide(mr[j]));
+            #pragma unroll 1
             for (int j = 0; j < m; j++)
                 if (cr[j] >= 0) gg = gcdq<i128>(gg, Num<V>::wide(cr[j]));
+            #pragma unroll 1
             for (int j = 0; j < g; j++) {
                 gg = gcdq<i128>(gg, Num<V>::wide(grl[j]));
                 gg = gcdq<i128>(gg, Num<V>::wide(grh[j]));
@@ -1065,8 +1075,11 @@ RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool sto
             red = gg == 0 ? 1 : gg;
             const i128 lim = (i128)INT64_MAX;
             bool over = (i128)q / red > lim || (res.e2e >= 0 && Num<V>::wide(res.e2e) / red > lim);
+            #pragma unroll 1
             for (int j = 0; j < g; j++) over = over || Num<V>::wide(grh[j]) / red > lim;
+            #pragma unroll 1
             for (int j = 0; j < p; j++) over = over || (mr[j] >= 0 && Num<V>::wide(mr[j]) / red > lim);
+            #pragma unroll 1
             for (int j = 0; j < m; j++) over = over || (cr[j] >= 0 && Num<V>::wide(cr[j]) / red > lim);
             if (over) {
                 c.esc = 1; /* not representable even reduced */
@@ -1105,6 +1118,7 @@ RT_NI bool report_pass(const TM &tm, SetCtx<V> &c, const OutPtrs<V> &o, bool sto
             }
         }
     }
+    #pragma unroll 1
     for (; k < c.n; k++) {
         if (tm.leader()) {
             o.e2e[k] = RTGPU_ABSENT;
@@ -1139,6 +1153,7 @@ RT_NI int find_g(const TM &tm, SetCtx<V> &c, int k, int lo, int hi, typename Num
     if (lo >= hi) return 0;
     eval_task(tm, c, k, hi, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
     if (c.esc || !r.pass) return 0;
+    #pragma unroll 1
     while (hi - lo > 1) {
         int mid = lo + (hi - lo) / 2;
         eval_task(tm, c, k, mid, lcm_pre, false, r, (V *)nullptr, (V *)nullptr);
@@ -1156,8 +1171,10 @@ RT_NI int search_greedy(const TM &tm, SetCtx<V> &c) {
     typedef typename Num<V>::Qt Qt;
     Qt lcm_pre = 1;
     i64 used = 0, rest_min = 0;
+    #pragma unroll 1
     for (int k = 0; k < c.n; k++)
         if (c.TR()[k].isgpu) rest_min += c.TR()[k].gmin;
+    #pragma unroll 1
     for (int k = 0; k < c.n; k++) {
         TaskRec &t = c.TR()[k];
         if (!t.isgpu) {
@@ -1188,18 +1205,21 @@ template <class V, class TM>
 RT_NI int search_dfs(const TM &tm, SetCtx<V> &c) {
     typedef typename Num<V>::Qt Qt;
     int d = 0;
+    #pragma unroll 1
     for (;;) {
         if (d == c.n) return RTGPU_SCHEDULABLE;
         if (c.budget > 0 && c.evals >= c.budget) return RTGPU_UNDECIDED;
         TaskRec &t = c.TR()[d];
         Qt lcm_pre = 1;
         i64 used = 0, after = 0;
+        #pragma unroll 1
         for (int i = 0; i < d; i++)
             if (c.TR()[i].isgpu) {
                 lcm_pre = lcm_lim<Qt>(lcm_pre, (Qt)c.TR()[i].g, c.qlim);
                 if (lcm_pre == 0) return ST_ESCALATE;
                 used += c.TR()[i].g;
             }
+        #pragma unroll 1
         for (int i = d + 1; i < c.n; i++)
             if (c.TR()[i].isgpu) after += c.TR()[i].gmin;
         bool ok;
@@ -1221,14 +1241,17 @@ RT_NI int search_dfs(const TM &tm, SetCtx<V> &c) {
         }
         /* backtrack: the deepest earlier GPU task with room for one more SM
          * (it still passes: own-count monotone) */
+        #pragma unroll 1
         for (;;) {
             d--;
             if (d < 0) return RTGPU_UNSCHEDULABLE;
             TaskRec &b = c.TR()[d];
             if (!b.isgpu) continue;
             i64 u = 0, a = 0;
+            #pragma unroll 1
             for (int i = 0; i < d; i++)
                 if (c.TR()[i].isgpu) u += c.TR()[i].g;
+            #pragma unroll 1
             for (int i = d + 1; i < c.n; i++)
                 if (c.TR()[i].isgpu) a += c.TR()[i].gmin;
             if (b.g < c.GN - u - a) {
@@ -1267,6 +1290,7 @@ template <class V> RT_HD V max_susp_hi(const SetCtx<V> &c, const TaskRec &t, int
     const SegPtr ml_hi = sg + 2 * m + p, gw_hi = sg + 2 * m + 2 * p + g, gl = gw_hi + g, an = gl + g;
     typename Num<V>::Qt per = q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * gcount);
     V best = 0;
+    #pragma unroll 1
     for (int j = 0; j < g; j++) {
         V gr = (V)((i128)gw_hi[j] * an[j] - (i128)gl[j] * c.A) * (V)per + Num<V>::sc(gl[j], q);
         V m1 = c.mm == RTGPU_TWO_COPY ? Num<V>::sc(ml_hi[2 * j] + ml_hi[2 * j + 1], q)
@@ -1292,15 +1316,18 @@ template <class V> RT_HD bool susp_valid(const SetCtx<V> &c, const TaskRec &t, i
     };
     if (c.method == RTGPU_METHOD_BUSYWAIT) {
         V lo = Num<V>::sc(t.sCll + t.sMll, q), hi = Num<V>::sc(t.sClu + t.sMlu, q);
+        #pragma unroll 1
         for (int j = 0; j < g; j++) {
             lo += grl(j);
             hi += gru(j);
         }
         return lo <= hi && hi <= Num<V>::sc(t.T, q);
     }
+    #pragma unroll 1
     for (int j = 0; j < m; j++)
         if (cl_lo[j] > cl_hi[j]) return false;
     V sl_sum = 0;
+    #pragma unroll 1
     for (int j = 0; j < g; j++) {
         V lo, hi;
         if (c.mm == RTGPU_TWO_COPY) {
@@ -1342,6 +1369,7 @@ RT_NI V baseline_response(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt
     V r1 = (V)-1;
     if (!none) {
         V acc = sum_sh;
+        #pragma unroll 1
         for (int j = 0; j < t.m; j++) acc += outs[j];
         if (acc <= D) r1 = acc;
     }
@@ -1356,6 +1384,7 @@ template <class V> RT_HD typename Num<V>::Qt alloc_scale(SetCtx<V> &c) {
     typedef typename Num<V>::Qt Qt;
     Qt L = 1;
     bool any = false;
+    #pragma unroll 1
     for (int i = 0; i < c.n; i++)
         if (c.TR()[i].isgpu) {
             any = true;
@@ -1381,12 +1410,15 @@ RT_NI int eval_alloc_baseline(const TM &tm, SetCtx<V> &c, bool want_all, const O
     if (c.esc) return -2;
     c.vn = 0;
     ensure_views(tm, c, c.n, q);
+    #pragma unroll 1
     for (int i = 0; i < c.n; i++)
         if (!susp_valid(c, c.TR()[i], c.TR()[i].g, q)) return -1;
+    #pragma unroll 1
     for (int k = 0; k < c.n; k++) {
         c.evals++;
         V B = 0;
         if (c.method == RTGPU_METHOD_SELFSUSP)
+            #pragma unroll 1
             for (int i = 0; i < c.n; i++)
                 if (c.TR()[i].prio > c.TR()[k].prio) B = tmax(B, max_susp_hi(c, c.TR()[i], c.TR()[i].g, q));
         V r = baseline_response(tm, c, k, q, B, want_all);
@@ -1424,6 +1456,7 @@ RT_NI int eval_alloc_baseline(const TM &tm, SetCtx<V> &c, bool want_all, const O
 template <class V> RT_HD int min_valid_g(SetCtx<V> &c, int k, int lo) {
     typedef typename Num<V>::Qt Qt;
     const TaskRec &t = c.TR()[k];
+    #pragma unroll 1
     for (int g = lo; g <= c.GN; g++) {
         Qt q = (Qt)2 * (Qt)c.A * (Qt)g;
         if (q > c.qlim) {
@@ -1445,6 +1478,7 @@ template <class V> RT_HD int min_valid_g(SetCtx<V> &c, int k, int lo) {
 template <class V, class TM>
 RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
     int ids[RTGPU_MAX_TASKS], lower[RTGPU_MAX_TASKS], nid = 0;
+    #pragma unroll 1
     for (int k = 0; k < c.n; k++)
         if (c.TR()[k].isgpu) {
             int g = min_valid_g(c, k, c.TR()[k].gmin);
@@ -1454,12 +1488,15 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
             lower[nid++] = g;
         }
     i64 need = 0;
+    #pragma unroll 1
     for (int q = 0; q < nid; q++) need += lower[q];
     if (need > c.GN) return RTGPU_UNSCHEDULABLE;
     tm.sync();
     if (tm.leader())
+        #pragma unroll 1
         for (int q = 0; q < nid; q++) c.TR()[ids[q]].g = lower[q];
     tm.sync();
+    #pragma unroll 1
     for (;;) {
         if (c.budget > 0 && c.evals >= c.budget) return RTGPU_UNDECIDED;
         int f = eval_alloc_baseline(tm, c, false, (const OutPtrs<V> *)nullptr);
@@ -1475,12 +1512,14 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
                 Qt q = alloc_scale(c);
                 if (c.esc) return ST_ESCALATE;
                 V Bmin = 0;
+                #pragma unroll 1
                 for (int i = 0; i < c.n; i++) {
                     const TaskRec &t = c.TR()[i];
                     if (t.prio <= c.TR()[f].prio || !t.isgpu) continue;
                     const SegPtr sg = c.segs(t.seg);
                     const int m = t.m, p = t.p, g = m - 1;
                     const SegPtr ml_hi = sg + 2 * m + p, gl = sg + 2 * m + 2 * p + 2 * g;
+                    #pragma unroll 1
                     for (int j = 0; j < g; j++) {
                         i64 x = c.mm == RTGPU_TWO_COPY ? ml_hi[2 * j] + ml_hi[2 * j + 1] : ml_hi[j];
                         Bmin = tmax(Bmin, Num<V>::sc(x + gl[j], q));
@@ -1492,6 +1531,7 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
             }
             if (prefix_dead) {
                 pos = -1;
+                #pragma unroll 1
                 for (int q = 0; q < nid; q++)
                     if (ids[q] <= f) pos = q;
                 if (pos < 0) return RTGPU_UNSCHEDULABLE; /* fails before any choice */
@@ -1499,9 +1539,12 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
         }
         /* advance the odometer at pos (gpu.py:43 order) */
         int q = pos;
+        #pragma unroll 1
         for (; q >= 0; q--) {
             i64 used = 0, after = 0;
+            #pragma unroll 1
             for (int a = 0; a < q; a++) used += c.TR()[ids[a]].g;
+            #pragma unroll 1
             for (int a = q + 1; a < nid; a++) after += lower[a];
             if (c.TR()[ids[q]].g + 1 <= c.GN - used - after) break;
         }
@@ -1509,6 +1552,7 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
         tm.sync();
         if (tm.leader()) {
             c.TR()[ids[q]].g += 1;
+            #pragma unroll 1
             for (int a = q + 1; a < nid; a++) c.TR()[ids[a]].g = lower[a];
         }
         tm.sync();
@@ -1928,6 +1972,7 @@ RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 ho
         c.TR()[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
         c.TR()[i].g = 1;
     });
+    #pragma unroll 1
     for (int i = 0; i < c.n; i++) {
         if (c.TR()[i].flags & TF_UNSUP) return RTGPU_INVALID;
         vb_max = tmax(vb_max, (i128)c.TR()[i].B);
@@ -1940,6 +1985,7 @@ RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 ho
     tm.sync();
     tm.pfor(c.n, [&](int kk) {
         i64 b = 0;
+        #pragma unroll 1
         for (int i = 0; i < c.n; i++)
             if (c.TR()[i].prio > c.TR()[kk].prio) b = tmax(b, c.TR()[i].maxMlu);
         c.TR()[kk].B = b;
@@ -1969,6 +2015,7 @@ RT_NI int run_query(const TM &tm, SetCtx<V> &c, int kind, int k, int idx, i64 ho
         const int h0 = kind == RTGPU_Q_MAX_WORKLOAD ? 0 : idx;
         const int h1 = kind == RTGPU_Q_MAX_WORKLOAD ? p : idx + 1;
         if (h0 < 0 || h1 > p) return RTGPU_INVALID;
+        #pragma unroll 1
         for (int hh = h0; hh < h1; hh++) {
             V rho;
             V w = walk(view, PM, half, p, hh, H, rho, err);
@@ -2042,17 +2089,21 @@ RT_NI int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
             /* store the clamped bound temporarily in B (recomputed below) */
             c.TR()[i].B = vb > (i128)((i64)1 << 62) ? ((i64)1 << 62) : (i64)vb;
         });
+        #pragma unroll 1
         for (int i = 0; i < c.n; i++) vb_max = tmax(vb_max, (i128)c.TR()[i].B);
     }
+    #pragma unroll 1
     for (int k = 0; k < c.n; k++)
         if (c.TR()[k].flags & TF_UNSUP) return RTGPU_INVALID;
     /* reference order: the first task whose min-SM search raises or fails */
+    #pragma unroll 1
     for (int k = 0; k < c.n; k++) {
         if (c.TR()[k].flags & TF_INV) return RTGPU_INVALID;
         if (c.TR()[k].flags & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE;
     }
     i64 need = 0;
     bool irregular = false;
+    #pragma unroll 1
     for (int k = 0; k < c.n; k++) {
         if (c.TR()[k].isgpu) need += c.TR()[k].gmin;
         if (c.TR()[k].flags & TF_IRREG) irregular = true;
@@ -2067,6 +2118,7 @@ RT_NI int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
 #ifndef RTGPU_NO_FIXED_Q
     if (c.method == RTGPU_METHOD_RTGPU && c.GN >= 1 && c.GN <= 64) {
         Qt L = 1;
+        #pragma unroll 1
         for (int g = 2; g <= c.GN && L != 0; g++) L = lcm_lim<Qt>(L, (Qt)g, c.qlim);
         if (L != 0 && L <= c.qlim / (2 * (Qt)c.A)) c.fixed_q = L * 2 * (Qt)c.A;
     }
@@ -2075,6 +2127,7 @@ RT_NI int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
     /* mem blocking term of analysis.py:162: longest copy of any lower-priority task */
     tm.pfor(c.n, [&](int k) {
         i64 b = 0;
+        #pragma unroll 1
         for (int i = 0; i < c.n; i++)
             if (c.TR()[i].prio > c.TR()[k].prio) b = tmax(b, c.TR()[i].maxMlu);
         c.TR()[k].B = b;
@@ -2092,6 +2145,7 @@ RT_NI int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
              * lexicographically largest one (first GPU task takes the rest) */
             int first = -1;
             i64 others = 0;
+            #pragma unroll 1
             for (int k = 0; k < c.n; k++)
                 if (c.TR()[k].isgpu) {
                     if (first < 0) first = k;
@@ -2099,6 +2153,7 @@ RT_NI int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
                 }
             tm.sync();
             if (tm.leader())
+                #pragma unroll 1
                 for (int k = 0; k < c.n; k++)
                     c.TR()[k].g = c.TR()[k].isgpu ? (k == first ? (int)(c.GN - others) : c.TR()[k].gmin) : 0;
             tm.sync();
@@ -2110,6 +2165,7 @@ RT_NI int analyze_set(const TM &tm, SetCtx<V> &c, unsigned flags, const OutPtrs<
         } else {
             int f = eval_alloc_baseline(tm, c, true, &o);
             if (f >= 0) /* tasks after the first failing one are not in per_task */
+                #pragma unroll 1
                 for (int k = f + 1; k < c.n; k++)
                     if (tm.leader()) {
                         o.e2e[k] = RTGPU_ABSENT;
