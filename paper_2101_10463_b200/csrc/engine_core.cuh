@@ -416,6 +416,23 @@ struct WarpTeam {
         if (w == m && rho > a.rho) a.rho = rho;
         a.err = a.err || e;
     }
+    /* the group sum and the error vote only; acc_rho gives the slope-1
+     * length when the iteration continues (not on the converging one) */
+    template <class V>
+    __device__ __forceinline__ void acc_sum(int lg, const Acc<V> &a, V &wsum, bool &err) const {
+        V s = a.sum;
+        for (int off = 1 << lg; off < 32; off <<= 1) s += shfl_x(s, off);
+        wsum = s;
+        err = __any_sync(0xffffffffu, a.err);
+    }
+    template <class V> __device__ __forceinline__ V acc_rho(const Acc<V> &a) const {
+        V r = a.rho;
+        for (int off = 1; off < 32; off <<= 1) {
+            V o = shfl_x(r, off);
+            if (o > r) r = o;
+        }
+        return r;
+    }
     template <class V>
     __device__ __forceinline__ void acc_finish(int lg, Acc<V> &a, V &wsum, V &rhomax, bool &err) const {
         V s = a.sum;
@@ -467,6 +484,11 @@ struct SeqTeam {
                 if (w[s] == m && r[s] > a.rho) a.rho = r[s];
         }
     }
+    template <class V> RT_HD void acc_sum(int, const Acc<V> &a, V &wsum, bool &err) const {
+        wsum = a.sum;
+        err = a.err;
+    }
+    template <class V> RT_HD V acc_rho(const Acc<V> &a) const { return a.rho; }
     template <class V> RT_HD void acc_finish(int, Acc<V> &a, V &wsum, V &rhomax, bool &err) const {
         wsum = a.sum;
         rhomax = a.rho;
@@ -1701,13 +1723,13 @@ RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kin
                     }
                 }, acc);
             }
-        V I, rho;
+        V I;
         bool err;
-        tm.acc_finish(lg, acc, I, rho, err);
+        tm.acc_sum(lg, acc, I, err);
         if (err) return (V)-1;
         V nxt = base + I;
         if (nxt <= r) return r;
-        nxt += rho;
+        nxt += tm.acc_rho(acc);
         if (nxt > bound) return (V)-1;
         r = nxt;
     }
