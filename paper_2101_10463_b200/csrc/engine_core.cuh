@@ -1804,6 +1804,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     const bool lg_tab = GN <= c.L.scr_n - (c.MP + c.MC + 2) - 32;
     if (lg_tab) tm.pfor(GN, [&](int x) { outs[x] = (V)(L / (Qt)(x + 1)); });
     i64 used = 0, rest_min = need;
+    V mem_prev_b = -1, mem_prev_r = 0; /* last memory fixed point (base, value) */
     #pragma unroll 1
     for (int k = 0; k < n; k++) {
         const TaskRec &t = tr[k];
@@ -1831,9 +1832,18 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                 bsum_t += ml_hi[j] + t.B;
             }
             const V bmax = Num<V>::sc(bmax_t, q);
-            const V rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, bmax, D);
+            /* warm start across tasks: hp(k) grows with k, so the memory
+             * interference of task k is pointwise >= that of any earlier
+             * task, and lfp(b') >= lfp(b) + (b' - b) for b' >= b: the
+             * previous task's fixed point shifted by the base difference is
+             * below this one */
+            V start = bmax;
+            if (mem_prev_b >= 0 && bmax >= mem_prev_b) start = tmax(bmax, mem_prev_r + (bmax - mem_prev_b));
+            const V rmax = start > D ? (V)-1 : lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, start, D);
             if (rmax == (V)-2) return ST_ESCALATE;
             if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
+            mem_prev_b = bmax;
+            mem_prev_r = rmax;
             mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
         }
         V sum_cr = -1; /* not computed yet; -2: some CR is None */
