@@ -95,9 +95,12 @@ int scan_dims_host(const i64 *blobs, const i64 *set_off, i64 n_sets, Dims *d) {
  * (then int128): their latency, not their number, sets the stages' time,
  * and an FP64 general pass in between only lengthened the chain for the
  * hardest sets.  Other runs: FP64, int64, int128. */
+#ifndef RTGPU_VERDICT_I64_FIRST
+#define RTGPU_VERDICT_I64_FIRST 1
+#endif
 int launch_general(KParams &p, cudaStream_t st) {
     int rc = 0;
-    if (p.use_fast && !(p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) {
+    if (RTGPU_VERDICT_I64_FIRST && p.use_fast && !(p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) {
         p.last_stage = 2;
         rc = launch_stage_i64(p, 1, st);
         if (g_timing) cudaEventRecord(g_ev[2], st);
