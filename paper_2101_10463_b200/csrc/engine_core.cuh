@@ -1773,11 +1773,22 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         if (t.isgpu) need += t.gmin;
     }
     if (need > GN) return RTGPU_UNSCHEDULABLE;
-    /* one scale for the whole search: 2 * A * lcm(1..GN), if it fits */
+    /* One scale for the whole search: q = 2 * A * lcm(1..gtop).  Every
+     * count the search evaluates for task k lies in [gmin_k, gmin_k + slack]
+     * (slack = GN - sum of minimum counts: ghi = GN - used - rest_min <=
+     * GN - sum_{i != k} gmin_i), and the hp views use final counts from the
+     * same ranges, so every GR term's denominator divides 2 * A * g with
+     * g <= gtop = max_k min(GN, gmin_k + slack).  Usually far below GN (the
+     * benchmark: gtop 3-5 instead of 10), which keeps low-utilisation sets
+     * (long periods) inside FP64's exact range. */
     const i128 vb = (i128)vb_max * range_factor(n, c.MC, c.MP);
     if (vb > (i128)Num<V>::limit()) return ST_ESCALATE_RANGE;
     const Qt qlim = Num<V>::limit() / (Qt)vb;
-    const Qt L = lcm_upto(GN);
+    int gtop = 1;
+    #pragma unroll 1
+    for (int k = 0; k < n; k++)
+        if (tr[k].isgpu) gtop = tmax(gtop, (int)tmin((i64)GN, (i64)tr[k].gmin + (GN - need)));
+    const Qt L = lcm_upto(gtop);
     if (L == 0 || (i128)L * (2 * A) > (i128)qlim) return ST_ESCALATE_RANGE;
     const Qt q = L * 2 * A;
     c.Vb = (i64)vb;
