@@ -1756,7 +1756,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     c.vq = 0;
     c.esc = 0;
     c.evals = 0;
-    if (n < 1 || n > c.maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > 64)
+    if (n < 1 || n > c.maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > (1 << 20))
         return ST_ESCALATE;
     TaskRec *tr = c.TR();
     tm.pfor(n, [&](int i) { load_task_fast(c, i); });
@@ -1809,11 +1809,11 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     V *bases = c.SCR();
     V *outs = c.SCR() + (c.MP + c.MC + 2);
     int *ord = (int *)(c.SCR() + c.L.scr_n) - 32;
-    /* L / g for every count g (GR up = sInfl * L/g + GL at scale q): one
-     * lane-parallel division per set instead of a 64-bit division per
-     * evaluation; outs has room when GN <= scr_n - (MP + MC + 2) - 32 */
-    const bool lg_tab = GN <= c.L.scr_n - (c.MP + c.MC + 2) - 32;
-    if (lg_tab) tm.pfor(GN, [&](int x) { outs[x] = (V)(L / (Qt)(x + 1)); });
+    /* L / g for every count g <= gtop (GR up = sInfl * L/g + GL at scale
+     * q): one lane-parallel division per set instead of a 64-bit division
+     * per evaluation; outs has room when gtop <= scr_n - (MP + MC + 2) - 32 */
+    const bool lg_tab = gtop <= c.L.scr_n - (c.MP + c.MC + 2) - 32;
+    if (lg_tab) tm.pfor(gtop, [&](int x) { outs[x] = (V)(L / (Qt)(x + 1)); });
     i64 used = 0, rest_min = need;
     V mem_prev_b = -1, mem_prev_r = 0; /* last memory fixed point (base, value) */
     #pragma unroll 1

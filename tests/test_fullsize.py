@@ -23,9 +23,9 @@ from paper_2101_10463_b200 import _native  # noqa: E402
 GREEDY = 0x100
 
 
-def gen(n, m, gn, u, count, mm=0, seed0=0):
+def gen(n, m, gn, u, count, mm=0, seed0=0, compact=False):
     gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), Fraction(u), mm,
-                              gn, Fraction(12, 100), Fraction(1))
+                              gn, Fraction(12, 100), Fraction(1), compact=compact)
     return _native.generate(gp, list(range(seed0, seed0 + count)))
 
 
@@ -71,3 +71,37 @@ def test_gpu_full_size(n, m, u, count):
     batch.run(out, flags=1)
     g = out.to_host()
     same(greedy, {"status": g.status, "vsm": g.vsm, "e2e_num": g.e2e_num, "den": g.den})
+
+
+def same_verdicts(ref, status, vsm, task_base):
+    assert np.array_equal(ref["status"], status)
+    sched = np.repeat(ref["status"] == 1, np.diff(task_base))
+    assert np.array_equal(ref["vsm"][sched], vsm[sched])
+
+
+@pytest.mark.parametrize("n,m,u,count", [(16, 9, "1/5", 30), (16, 9, "1", 30),
+                                         (64, 5, "1", 6), (64, 5, "2", 6)])
+def test_engine_core_full_size_verdicts(n, m, u, count):
+    """Verdict runs on compact blobs at 148 SMs: the fast path takes the sets
+    whose candidate counts stay small enough for its fixed scale, the
+    general path the rest; both agree with the greedy oracle."""
+    b, so, tb = gen(n, m, 148, u, count, compact=True)
+    greedy = oracle.analyze_batch(b, so, tb, flags=1 | GREEDY, threads=8, detail=False)
+    h = harness.analyze_batch(b, so, tb, flags=0, detail=False)
+    same_verdicts(greedy, h["status"], h["vsm"], tb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,u,count", [(16, 9, "1/5", 200), (16, 9, "1", 100),
+                                         (64, 5, "1", 30), (64, 5, "2", 30)])
+def test_gpu_full_size_verdicts(n, m, u, count):
+    from paper_2101_10463_b200.engine import DeviceBatch, analyze_packed
+    b, so, tb = gen(n, m, 148, u, count, seed0=91, compact=True)
+    greedy = oracle.analyze_batch(b, so, tb, flags=1 | GREEDY, threads=16, detail=False)
+    batch = DeviceBatch(b, so, tb)
+    out = batch.alloc_results()
+    batch.run(out, flags=0)
+    g = out.to_host()
+    same_verdicts(greedy, g.status, g.vsm, tb)
+    h = analyze_packed(b, so, tb, 0, 0)  # the streamed end-to-end path
+    same_verdicts(greedy, h.status, h.vsm, tb)
