@@ -210,8 +210,11 @@ __device__ __forceinline__ void wait_chunk(const KParams &p, i64 s, int lane) {
  * and nothing else, so neither the general path's stack frame and
  * registers nor its code sit in this kernel -- sets it cannot decide go to
  * stage 1's list like the front kernel's escalations. */
+#ifndef RTGPU_FAST_MINB
+#define RTGPU_FAST_MINB RTGPU_MINB
+#endif
 template <bool STREAM>
-__global__ void __launch_bounds__(256, MinBlocks<double>::value) fast_kernel(KParams p) {
+__global__ void __launch_bounds__(256, RTGPU_FAST_MINB) fast_kernel(KParams p) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     Layout<double> L;
