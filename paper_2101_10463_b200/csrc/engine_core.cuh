@@ -1622,27 +1622,22 @@ RT_NI void load_task_fast(SetCtx<V> &c, int i) {
     }
     const Seg32 sg{(const int32_t *)c.blob + t.seg}; /* compact blob (checked by the caller) */
     i64 clu = 0, cll = 0, mlu = 0, mll = 0, gwl = 0, infl = 0, gls = 0, inner = 0, mx = 0, ih = 0;
-    {
-        /* every value must be non-negative: one OR per value, then the sign */
-        int32_t acc = 0;
-        #pragma unroll 1
-        for (int j = 0; j < 2 * m + 2 * p + 4 * g; j++) acc |= sg.p[j];
-        if (acc < 0) {
-            t.flags = TF_UNSUP;
-            t.B = 0;
-            return;
-        }
-    }
+    /* one pass over the area: the sums, and an OR of every value whose sign
+     * says whether any is negative (then the set is not for the fast path) */
+    i64 acc = 0;
     #pragma unroll 1
     for (int j = 0; j < m; j++) {
-        clu += sg[m + j];
-        cll += sg[j];
-        if (j >= 1 && j <= m - 2) inner += sg[j];
+        const i64 lo = sg[j], hi = sg[m + j];
+        acc |= lo | hi;
+        clu += hi;
+        cll += lo;
+        if (j >= 1 && j <= m - 2) inner += lo;
     }
     #pragma unroll 1
     for (int j = 0; j < p; j++) {
-        mll += sg[2 * m + j];
-        const i64 h = sg[2 * m + p + j];
+        const i64 lo = sg[2 * m + j], h = sg[2 * m + p + j];
+        acc |= lo | h;
+        mll += lo;
         mlu += h;
         mx = tmax(mx, h);
     }
@@ -1650,12 +1645,18 @@ RT_NI void load_task_fast(SetCtx<V> &c, int i) {
     for (int j = 0; j < g; j++) {
         const i64 lo = sg[2 * m + 2 * p + j], hi = sg[2 * m + 2 * p + g + j];
         const i64 gl = sg[2 * m + 2 * p + 2 * g + j], an = sg[2 * m + 2 * p + 3 * g + j];
+        acc |= lo | hi | gl | an;
         const i64 w = hi * an, o = gl * c.A; /* < 2^47 */
         if (o > w) t.flags |= TF_INV;
         infl += w - o;
         ih += w;
         gls += gl;
         gwl += lo;
+    }
+    if (acc < 0) {
+        t.flags = TF_UNSUP;
+        t.B = 0;
+        return;
     }
     t.sClu = clu;
     t.sCll = cll;
