@@ -69,7 +69,10 @@ template <class V> struct Num;
 template <> struct Num<double> {
     typedef i64 Qt;
     static RT_HD i64 limit() { return (i64)1 << 52; }
-    static RT_HD double sc(i64 x, i64 q) { return (double)(x * q); }
+    /* x * q as an exact double: both factors are exact (< 2^53) and the
+     * stage's range check keeps every product below 2^52, so one DMUL
+     * replaces a 64-bit integer multiply and its conversion */
+    static RT_HD double sc(i64 x, i64 q) { return (double)x * (double)q; }
     static RT_HD double of(i64 x) { return (double)x; }
     static RT_HD double floordiv(double a, double b) {
         double q = floor(a / b);
