@@ -1708,7 +1708,6 @@ RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kin
                  int PM, int half, int stride, V base, V start, V bound) {
     if (base > bound) return (V)-1;
     RT_COUNT(g_cnt_flfp[kind]);
-    const i64 prio_k = tr[k].prio;
     V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
         RT_COUNT(g_cnt_fit[kind]);
@@ -1720,10 +1719,11 @@ RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kin
                 tm.group_max_round(lg, [&](int slot, V &w, V &rr, bool &es) {
                     int i = i0 + (slot >> lg), h = slot & ((1 << lg) - 1);
                     if (i < k) {
+                        /* hp(k) = tasks 0..k-1: fast_verdict admits only
+                         * strictly increasing priorities */
                         const TaskRec &ti = tr[i];
                         int p = kind == K_CPU ? ti.m : ti.p;
-                        if (h < p && ti.prio < prio_k)
-                            w = walk(views + (size_t)i * stride, PM, half, p, h, r, rr, es);
+                        if (h < p) w = walk(views + (size_t)i * stride, PM, half, p, h, r, rr, es);
                     }
                 }, acc);
             }
@@ -1767,7 +1767,8 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     i64 vb_max = 0, need = 0;
     #pragma unroll 1
     for (int k = 0; k < n; k++)
-        if (tr[k].flags & (TF_UNSUP | TF_IRREG)) return ST_ESCALATE;
+        if ((tr[k].flags & (TF_UNSUP | TF_IRREG)) || (k > 0 && tr[k].prio <= tr[k - 1].prio))
+            return ST_ESCALATE; /* (equal priorities: the general path) */
     #pragma unroll 1
     for (int k = 0; k < n; k++) {
         const TaskRec &t = tr[k];
