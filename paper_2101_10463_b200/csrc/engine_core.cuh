@@ -603,6 +603,103 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
     }
 }
 
+#ifdef __CUDA_ARCH__
+/* build_view for the verdict fast path (compact blobs, RTGPU chains), with
+ * the segments spread over the lanes: lane j holds segment j's length and
+ * the gap after it, and the prefix sums P (segment + gap) and EP (segment)
+ * are two warp scans -- instead of one lane walking the chain while 31
+ * wait.  Integer-valued doubles below 2^52: the sums are exact in any
+ * order, so the view is identical to build_view's. */
+template <class V>
+__device__ __noinline__ void build_view_warp(SetCtx<V> &c, int i, i64 q, int lane) {
+    typedef Num<V> N;
+    const TaskRec &t = c.TR()[i];
+    const Seg32 sg{(const int32_t *)c.blob + t.seg};
+    const int m = t.m, p = t.p;
+    const Seg32 cl_lo = sg, cl_hi = sg + m, ml_lo = sg + 2 * m, ml_hi = ml_lo + p;
+    const Seg32 gw_lo = ml_hi + p;
+    const i64 perlo = t.isgpu ? q / (2 * (i64)t.g) : q;
+    const V vper = (V)perlo;
+    const bool two = c.mm == RTGPU_TWO_COPY;
+    /* CPU chain */
+    {
+        VOff o(c.MC);
+        V *v = c.VC() + (size_t)i * c.L.SC;
+        V e = 0, gap = 0;
+        if (lane < m) {
+            e = N::sc(cl_hi[lane], q);
+            if (lane < m - 1)
+                gap = (two ? N::sc(ml_lo[2 * lane] + ml_lo[2 * lane + 1], q) : N::sc(ml_lo[lane], q)) +
+                      (V)gw_lo[lane] * vper;
+        }
+        V s1 = e + gap, s2 = e;
+        #pragma unroll 1
+        for (int off = 1; off < m; off <<= 1) {
+            const V a1 = __shfl_up_sync(0xffffffffu, s1, off), a2 = __shfl_up_sync(0xffffffffu, s2, off);
+            if (lane >= off) {
+                s1 += a1;
+                s2 += a2;
+            }
+        }
+        if (lane < m) {
+            const V P = s1 - e - gap, EP = s2 - e;
+            v[o.e + lane] = e;
+            v[o.P + lane] = P;
+            v[o.EP + lane] = EP;
+            if (lane == m - 1) {
+                v[o.EP + m] = s2;
+                v[o.F1] = P + e + N::sc(t.T - t.D, q);
+                const V wrap = N::sc(t.T - t.sClu - t.sMll, q) - (t.isgpu ? (V)t.sGWlo * vper : (V)0);
+                v[o.WN] = wrap < 0 ? (V)1 : (V)0;
+                v[o.P + m] = P + e + (wrap < 0 ? (V)0 : wrap);
+                v[o.INV] = N::make_inv(v[o.P + m]);
+            }
+        }
+    }
+    /* memory chain */
+    if (p > 0) {
+        VOff o(c.MP);
+        V *v = c.VM() + (size_t)i * c.L.SM;
+        V e = 0, gap = 0;
+        if (lane < p) {
+            e = N::sc(ml_hi[lane], q);
+            if (lane < p - 1) {
+                if (two)
+                    gap = (lane % 2 == 0) ? (V)gw_lo[lane / 2] * vper : N::sc(cl_lo[(lane + 1) / 2], q);
+                else
+                    gap = (V)gw_lo[lane] * vper + N::sc(cl_lo[lane + 1], q);
+            }
+        }
+        V s1 = e + gap, s2 = e;
+        #pragma unroll 1
+        for (int off = 1; off < p; off <<= 1) {
+            const V a1 = __shfl_up_sync(0xffffffffu, s1, off), a2 = __shfl_up_sync(0xffffffffu, s2, off);
+            if (lane >= off) {
+                s1 += a1;
+                s2 += a2;
+            }
+        }
+        if (lane < p) {
+            const V P = s1 - e - gap, EP = s2 - e;
+            v[o.e + lane] = e;
+            v[o.P + lane] = P;
+            v[o.EP + lane] = EP;
+            if (lane == p - 1) {
+                v[o.EP + p] = s2;
+                V first = N::sc(t.T - t.D + cl_lo[m - 1] + cl_lo[0], q);
+                if (!two) first += (V)gw_lo[m - 2] * vper;
+                v[o.F1] = P + e + first;
+                const V wrap = N::sc(t.T - t.sMlu - t.innerCll, q) - (V)t.sGWlo * vper;
+                v[o.WN] = wrap < 0 ? (V)1 : (V)0;
+                v[o.P + p] = P + e + (wrap < 0 ? (V)0 : wrap);
+                v[o.INV] = N::make_inv(v[o.P + p]);
+            }
+        }
+    }
+    __syncwarp();
+}
+#endif
+
 /* Views of tasks [0, k) at scale q (reused when already current). */
 template <class V, class TM>
 RT_HD void ensure_views(const TM &tm, SetCtx<V> &c, int k, typename Num<V>::Qt q) {
@@ -1825,7 +1922,11 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     for (int k = 0; k < n; k++) {
         const TaskRec &t = tr[k];
         /* views of tasks before k (their counts are final) */
+#ifdef __CUDA_ARCH__
+        if (k > 0) build_view_warp(c, k - 1, q, tm.lane);
+#else
         if (k > 0) tm.pfor(1, [&](int) { build_view<V, Seg32>(c, k - 1, q); });
+#endif
         const Seg32 sg{(const int32_t *)c.blob + t.seg};
         const Seg32 cl_hi = sg + t.m, ml_hi = sg + 2 * t.m + t.p;
         const V D = Num<V>::sc(t.D, q);
