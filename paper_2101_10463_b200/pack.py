@@ -132,20 +132,31 @@ def lcm_denominators(values) -> int:
     return _lcm_all(Fraction(v).denominator for v in values)
 
 
+def _den(x) -> int:
+    """Denominator of an int / Fraction duration without building a Fraction."""
+    d = getattr(x, "denominator", None)
+    return d if d is not None else Fraction(x).denominator
+
+
 def pack_set(ts: TaskSet) -> tuple[list[int], int, tuple]:
     """One blob as a list of Python ints plus its time scale and task order."""
     _check_shape(ts)
-    S = _lcm_all(Fraction(d).denominator for d in _durations(ts))
-    A = _lcm_all(Fraction(g.interleave_ratio).denominator
-                 for t in ts.tasks for g in t.gpu_segments)
+    S = _lcm_all(_den(d) for d in _durations(ts))
+    A = _lcm_all(_den(g.interleave_ratio) for t in ts.tasks for g in t.gpu_segments)
     order = ts.by_priority()
     index_of = {id(t): i for i, t in enumerate(ts.tasks)}
     n = len(order)
 
     def tick(x) -> int:
-        v = Fraction(x) * S
-        assert v.denominator == 1
-        return int(v)
+        # x * S exactly: S is a multiple of x's denominator (integer
+        # arithmetic, no Fraction objects on the hot path of bulk packing)
+        num, den = getattr(x, "numerator", None), getattr(x, "denominator", None)
+        if num is None:
+            f = Fraction(x)
+            num, den = f.numerator, f.denominator
+        q, r = divmod(S, den)
+        assert r == 0
+        return num * q
 
     header = [n, ts.platform.physical_sms,
               0 if ts.mem_model is MemModel.TWO_COPY else 1, A, 0,
@@ -166,8 +177,12 @@ def pack_set(ts: TaskSet) -> tuple[list[int], int, tuple]:
         segs += [tick(g.work.hi) for g in t.gpu_segments]
         segs += [tick(g.critical_path_overhead) for g in t.gpu_segments]
         for g in t.gpu_segments:
-            a = Fraction(g.interleave_ratio) * A
-            segs.append(int(a))
+            r = g.interleave_ratio
+            num, den = getattr(r, "numerator", None), getattr(r, "denominator", None)
+            if num is None:
+                f = Fraction(r)
+                num, den = f.numerator, f.denominator
+            segs.append(num * (A // den))
     blob = header + records + segs
     blob[4] = len(blob)
     for v in blob:
