@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if ((i64)idx >= count) break;
         const i64 s = list[idx];
+        if (s < 0) continue; /* decided by stage 1a (the int64 fast path) */
         c.blob = p.blobs + p.set_off[s];
         const i64 tb = p.task_base[s];
         OutPtrs<V> o;
@@ -114,6 +115,50 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) analyze_kernel(KPara
         if (lane == 0) {
             p.status[s] = st;
             p.evals[s] = c.evals;
+        }
+        __syncwarp();
+    }
+}
+
+/* Stage 1a (verdict runs): the fast path in int64 over stage 0's
+ * escalations.  With the fixed scale from the candidate counts (gtop) the
+ * only sets stage 0 still escalates are range escalations (a handful per
+ * 100 000: periods so long that the FP64 scale does not fit), which the
+ * int64 instance decides in fast-path time instead of a general-path
+ * latency; it is a separate kernel so the FP64 fast kernel keeps its
+ * registers.  Decided entries of stage 0's list become -1 and the general
+ * stage skips them. */
+template <class V>
+__global__ void __launch_bounds__(256, MinBlocks<V>::value) fast_list_kernel(KParams p) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    Layout<V> L;
+    L.init(p.dims);
+    SetCtx<V> c;
+    kernel_ctx(c, p.dims, L, warp);
+    c.budget = p.budget;
+    c.method = p.method;
+    WarpTeam tm{lane};
+    const i64 count = (i64)p.ctr[4];
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(&p.ctr[7], 1ull);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if ((i64)idx >= count) break;
+        const i64 s = p.esc[0][idx];
+        c.blob = p.blobs + p.set_off[s];
+        const i64 tb = p.task_base[s];
+        const int st = fast_verdict(tm, c, p.vsm + tb);
+        if (st == ST_ESCALATE || st == ST_ESCALATE_RANGE) continue; /* the general stage's */
+        if (st != RTGPU_SCHEDULABLE) {
+            const int n = (int)c.blob[0];
+            for (int i = lane; i < n; i += 32) p.vsm[tb + i] = 0; /* no allocation */
+        }
+        __syncwarp();
+        if (lane == 0) {
+            p.status[s] = st;
+            p.evals[s] = c.evals;
+            p.esc[0][idx] = -1;
         }
         __syncwarp();
     }
@@ -399,6 +444,19 @@ template <class V> inline int launch_stage(const KParams &p, int stage, cudaStre
                              "analyze_kernel launch", p, stage, false);
 }
 
+template <class V> inline int launch_fast_list(const KParams &p, cudaStream_t st) {
+    int bytes = 0;
+    const int wpb = warps_per_block<V>(p.dims, &bytes);
+    if (wpb == 0) return 0; /* the general stage takes the list */
+    /* persistent over the list (its length is on the device): a few CTAs
+     * suffice, the list is short */
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return launch_persistent((void *)fast_list_kernel<V>, p.dims, 0, (i64)sms, wpb, bytes, st,
+                             "fast_list_kernel launch", p, 0, true);
+}
+
 #ifdef RTGPU_FRONT_TU
 inline int launch_front(const KParams &p, cudaStream_t st) {
     int bytes = 0;
@@ -446,6 +504,7 @@ int launch_query_i128(const QParams &p, int stage, cudaStream_t st);
 int launch_front_f64(const KParams &p, cudaStream_t st);
 int launch_stage_f64(const KParams &p, int stage, cudaStream_t st);
 int launch_stage_i64(const KParams &p, int stage, cudaStream_t st);
+int launch_fast_list_i64(const KParams &p, cudaStream_t st);
 int launch_stage_i128(const KParams &p, int stage, cudaStream_t st);
 
 }  // namespace rtgpu

@@ -102,7 +102,8 @@ int launch_general(KParams &p, cudaStream_t st) {
     int rc = 0;
     if (RTGPU_VERDICT_I64_FIRST && p.use_fast && !(p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) {
         p.last_stage = 2;
-        rc = launch_stage_i64(p, 1, st);
+        rc = launch_fast_list_i64(p, st); /* stage 1a: range escalations in int64 */
+        if (!rc) rc = launch_stage_i64(p, 1, st);
         if (g_timing) cudaEventRecord(g_ev[2], st);
         if (!rc) rc = launch_stage_i128(p, 2, st);
     } else {
@@ -431,7 +432,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
             r.esc[0] = p.esc[2];
             cudaMemcpyAsync(p.ctr + 4, p.ctr + 6, 8, cudaMemcpyDeviceToDevice, cs); /* list length */
             cudaMemsetAsync(p.ctr + 1, 0, 8 * 2, cs);                             /* work counters */
-            cudaMemsetAsync(p.ctr + 5, 0, 8 * 2, cs);                             /* later lists */
+            cudaMemsetAsync(p.ctr + 5, 0, 8 * 3, cs); /* later lists, stage-1a counter */
             r.esc[1] = p.esc[1];
             r.esc[2] = p.esc[0]; /* free now */
             rc = launch_general(r, cs);
