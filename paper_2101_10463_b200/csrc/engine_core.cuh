@@ -1857,8 +1857,9 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     c.vq = 0;
     c.esc = 0;
     c.evals = 0;
-    if (n < 1 || n > c.maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > (1 << 20))
-        return ST_ESCALATE;
+    if (n < 1 || n > c.maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > 64)
+        return ST_ESCALATE; /* GN > 64: the fixed scale almost never fits (gtop > 42); skip the
+                             * task loads and take the general path's per-task scales */
     TaskRec *tr = c.TR();
     tm.pfor(n, [&](int i) { load_task_fast(c, i); });
     i64 vb_max = 0, need = 0;
