@@ -229,7 +229,10 @@ __global__ void __launch_bounds__(256, MinBlocks<double>::value) front_kernel(KP
  * chunk's last set, loaded before this chunk's bytes arrived, and the
  * acquire invalidates it.  Lines of any other set lie wholly in its chunk and
  * are never loaded before the chunk's flag is seen. */
-__device__ __forceinline__ void wait_chunk(const KParams &p, i64 s, int lane) {
+__device__ __forceinline__ bool wait_chunk(const KParams &p, i64 s, int lane) {
+    /* bounded: a chunk that never arrives (a failed copy) must not hang the
+     * GPU -- after ~2^23 polls (seconds) the set is reported undecided */
+    int ok = 1;
     if (lane == 0) {
         const i64 n = p.n_sets, C = p.chunks;
         i64 c = s * C / n;
@@ -240,15 +243,19 @@ __device__ __forceinline__ void wait_chunk(const KParams &p, i64 s, int lane) {
         unsigned long long v;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
         if (v != p.epoch || first) {
-            for (;;) {
+            for (int polls = 0;; polls++) {
                 asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
                 if (v == p.epoch) break;
+                if (polls > (1 << 23)) {
+                    ok = 0;
+                    break;
+                }
                 __nanosleep(256);
             }
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
     }
-    __syncwarp();
+    return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 
 /* Stage 0 when the fast path applies (RTGPU, verdict only): the fast path
@@ -276,7 +283,11 @@ __global__ void __launch_bounds__(256, RTGPU_FAST_MINB) fast_kernel(KParams p) {
         if ((i64)idx >= p.n_sets) break;
         const i64 s = p.set_base + (i64)idx;
         if (STREAM) {
-            wait_chunk(p, s, lane);
+            if (!wait_chunk(p, s, lane)) {
+                if (lane == 0) p.status[s] = RTGPU_UNDECIDED;
+                __syncwarp();
+                continue;
+            }
             /* the layout was sized from a sample of the batch: a set beyond
              * it goes to the oversize list (esc[2], unused by verdict runs)
              * and the host re-runs it with the batch's true dims */
