@@ -13,6 +13,7 @@
  * A stage appends the sets whose exact scaled range it cannot hold to the
  * next stage's list; the next stage reads the count from device memory.
  */
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <string.h>
@@ -71,6 +72,25 @@ cudaEvent_t g_ev[4];
 bool g_ev_init = false;
 bool g_ev_valid = false;
 DevBuf g_h_blobs, g_h_off, g_h_tb, g_h_status, g_h_evals, g_h_vsm, g_h_e2e, g_h_den, g_h_detail;
+
+typedef CUresult (*WriteValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+/* cuStreamWriteValue64 through the runtime's driver entry point (no link
+ * against libcuda, so the library still loads on a machine without a GPU) */
+WriteValue64 write_value64() {
+    static WriteValue64 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (WriteValue64)p;
+        cudaGetLastError();
+    }
+    return fn;
+}
 
 int scan_dims_host(const i64 *blobs, const i64 *set_off, i64 n_sets, Dims *d) {
     d->maxn = 1;
@@ -393,7 +413,11 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
             const i64 a = n_sets * c / chunks, b = n_sets * (c + 1) / chunks;
             const size_t w0 = (size_t)set_off[a], w1 = (size_t)set_off[b];
             cudaMemcpyAsync((i64 *)g_h_blobs.p + w0, blobs + w0, (w1 - w0) * 8, cudaMemcpyHostToDevice, cp);
-            cudaMemcpyAsync(flags_d + c, h_epoch, 8, cudaMemcpyHostToDevice, cp);
+            /* the arrival flag: a stream memory operation when the driver
+             * exposes one (no copy-engine job per chunk), else an 8-byte copy */
+            if (!write_value64() ||
+                write_value64()((CUstream)cp, (CUdeviceptr)(flags_d + c), epoch, 0) != CUDA_SUCCESS)
+                cudaMemcpyAsync(flags_d + c, h_epoch, 8, cudaMemcpyHostToDevice, cp);
         }
         KParams q = p;
         q.set_base = 0;
