@@ -409,7 +409,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         cudaMemsetAsync(p.ctr, 0, 8 * 8, cs); /* stage counters, before the kernel */
         cudaMemcpyAsync(g_h_off.p, set_off, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
         cudaMemcpyAsync(g_h_tb.p, task_base, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
-        for (int c = 0; c < chunks; c++) {
+        auto enqueue_chunk = [&](int c) {
             const i64 a = n_sets * c / chunks, b = n_sets * (c + 1) / chunks;
             const size_t w0 = (size_t)set_off[a], w1 = (size_t)set_off[b];
             cudaMemcpyAsync((i64 *)g_h_blobs.p + w0, blobs + w0, (w1 - w0) * 8, cudaMemcpyHostToDevice, cp);
@@ -418,7 +418,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
             if (!write_value64() ||
                 write_value64()((CUstream)cp, (CUdeviceptr)(flags_d + c), epoch, 0) != CUDA_SUCCESS)
                 cudaMemcpyAsync(flags_d + c, h_epoch, 8, cudaMemcpyHostToDevice, cp);
-        }
+        };
         KParams q = p;
         q.set_base = 0;
         q.n_sets = n_sets;
@@ -426,7 +426,12 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         q.chunk_flag = flags_d;
         q.epoch = epoch;
         q.chunks = chunks;
+        /* the first chunk, then the kernel, then the rest: the kernel starts
+         * as soon as chunk 0 lands instead of after the host has enqueued
+         * every copy */
+        enqueue_chunk(0);
         int rc = launch_front_f64(q, cs);
+        for (int c = 1; c < chunks; c++) enqueue_chunk(c);
         if (!rc) {
             /* every chunk has arrived once the fast kernel is done */
             cudaEventRecord(g_ev_chunk[0], cp);
