@@ -117,8 +117,12 @@ int rtgpu_device_info(int *n_devices, int *sm_count, int *cc_major, int *cc_mino
  * Host pointers: the call copies the batch to the current device in chunks
  * overlapped with the analysis of the chunks already resident, and copies
  * the results back (the end-to-end path; pass pinned host memory for the
- * overlap).  e2e_num / den are written only with RTGPU_F_BOUNDS or
- * RTGPU_F_DETAIL.
+ * overlap).  Verdict runs (flags 0, RTGPU method) stream: one persistent
+ * kernel starts after the first chunk and waits per set on device-side
+ * arrival flags the copy stream writes; its shared-memory layout is sized
+ * from a sample of the batch and sets beyond it are re-run at the batch's
+ * true sizes.  Other runs pipeline per-chunk launches over two streams.
+ * e2e_num / den are written only with RTGPU_F_BOUNDS or RTGPU_F_DETAIL.
  * eval_budget <= 0 means unlimited.  Returns 0 or a negative error code.
  */
 int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off,
