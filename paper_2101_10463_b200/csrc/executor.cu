@@ -134,14 +134,20 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
     const int lane = threadIdx.x & 31;
     const long long witems = a.items * (long long)(blockDim.x >> 5);
     float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f;
-    unsigned long long it = 0;
-    if (lane == 0) it = claim(&a.ctl->work);
+    /* two claims in flight: a claim is consumed two items after it was
+     * issued, so an atomic delayed by copy traffic at the L2 (up to two
+     * items of compute) does not stall the warp */
+    unsigned long long it = 0, nx = 0;
+    if (lane == 0) {
+        it = claim(&a.ctl->work);
+        nx = claim(&a.ctl->work);
+    }
     it = __shfl_sync(0xffffffffu, it, 0);
     unsigned done = 0;
     while ((long long)it < witems) {
         done++;
-        unsigned long long nx = 0;
-        if (lane == 0) nx = claim(&a.ctl->work); /* in flight during the loop */
+        unsigned long long nn = 0;
+        if (lane == 0) nn = claim(&a.ctl->work); /* in flight for two items */
         const int iters = a.iters;
 #pragma unroll 4
         for (int k = 0; k < iters; k++) {
@@ -150,6 +156,7 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
             x2 = fmaf(x2, 0.9999999f, 0.5f);
         }
         it = __shfl_sync(0xffffffffu, nx, 0);
+        nx = nn;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
