@@ -231,9 +231,27 @@ struct SegPtr {
 /* The compact (int32) segment area with the width known at compile time:
  * the verdict fast path runs only on compact blobs, so its reads are plain
  * 32-bit loads with no per-access width select. */
+#if defined(__CUDA_ARCH__) && defined(RTGPU_BLOB_EVICT_FIRST)
+/* batch words are read once per set: an L2 evict-first hint keeps the stream
+ * of them from evicting the warps' (dirty) local-memory lines, whose
+ * write-backs otherwise double the kernel's DRAM traffic */
+__device__ __forceinline__ int32_t ld_batch32(const int32_t *a) {
+    int32_t v;
+    asm("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "ld.global.L2::cache_hint.b32 %0, [%1], pol;\n\t}"
+        : "=r"(v)
+        : "l"(__cvta_generic_to_global(a)));
+    return v;
+}
+#endif
+
 struct Seg32 {
     const int32_t *p;
+#if defined(__CUDA_ARCH__) && defined(RTGPU_BLOB_EVICT_FIRST)
+    __device__ i64 operator[](int j) const { return ld_batch32(p + j); }
+#else
     RT_HD i64 operator[](int j) const { return p[j]; }
+#endif
     RT_HD Seg32 operator+(int j) const { return Seg32{p + j}; }
 };
 

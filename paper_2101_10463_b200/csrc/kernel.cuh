@@ -42,6 +42,9 @@ struct KParams {
      * n*c/chunks <= s < n*(c+1)/chunks is readable once chunk_flag[c] ==
      * epoch (the copy stream writes it after the chunk's H2D copy) */
     const unsigned long long *chunk_flag = nullptr;
+    /* set to epoch by the first warp whose wait times out: every other warp
+     * then stops waiting at once and the host re-runs the batch unstreamed */
+    unsigned long long *chunk_abort = nullptr;
     unsigned long long epoch = 0;
     int chunks = 1;
     i64 set_base;              /* front stage: first set of this launch (chunked e2e path) */
@@ -246,7 +249,11 @@ __device__ __forceinline__ bool wait_chunk(const KParams &p, i64 s, int lane) {
             for (int polls = 0;; polls++) {
                 asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
                 if (v == p.epoch) break;
-                if (polls > (1 << 23)) {
+                unsigned long long a;
+                asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(a) : "l"(p.chunk_abort) : "memory");
+                if (a == p.epoch || polls > (1 << 22)) {
+                    if (a != p.epoch)
+                        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.chunk_abort), "l"(p.epoch) : "memory");
                     ok = 0;
                     break;
                 }

@@ -61,7 +61,7 @@ DevBuf g_scratch; /* counters + escalation lists */
 const int MAX_CHUNKS = 32;
 /* [0..7] stage counters, [8, 8 + MAX_CHUNKS) per-chunk work counters,
  * [8 + MAX_CHUNKS, 8 + 2 MAX_CHUNKS) chunk arrival flags (streamed path) */
-const size_t CTR_WORDS = 8 + 2 * MAX_CHUNKS;
+const size_t CTR_WORDS = 9 + 2 * MAX_CHUNKS; /* [8+2*MAX_CHUNKS]: stream abort word */
 cudaStream_t g_s_copy = nullptr, g_s_comp[2] = {nullptr, nullptr};
 cudaEvent_t g_ev_chunk[MAX_CHUNKS], g_ev_comp[2];
 bool g_pipe_init = false;
@@ -390,7 +390,14 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
     p.esc[1] = p.esc[0] + n_sets;
     p.esc[2] = p.esc[1] + n_sets;
     p.use_fast = flags == 0 && method == RTGPU_METHOD_RTGPU;
-    if (p.use_fast && !(flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) {
+    /* RTGPU_NO_STREAM=1 forces the chunked-launch path: under a profiler that
+     * serialises kernels (ncu) the persistent streamed kernel would wait for
+     * copies queued behind it */
+    static const bool no_stream = [] {
+        const char *v = getenv("RTGPU_NO_STREAM");
+        return v && v[0] == '1';
+    }();
+    if (p.use_fast && !no_stream && !(flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) {
         /* Verdict runs stream: ONE persistent fast kernel runs while the copy
          * stream moves the batch chunk by chunk; after each chunk the copy
          * stream writes the call's epoch into that chunk's arrival flag and
@@ -424,6 +431,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         q.n_sets = n_sets;
         q.wctr0 = &p.ctr[0];
         q.chunk_flag = flags_d;
+        q.chunk_abort = p.ctr + 8 + 2 * MAX_CHUNKS; /* epoch-valued: no reset needed */
         q.epoch = epoch;
         q.chunks = chunks;
         /* the first chunk, then the kernel, then the rest: the kernel starts
@@ -443,39 +451,48 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
          * learns their count, scans the true dims and runs them through the
          * general stages as stage 0's escalations */
         static unsigned long long *h_over = nullptr;
-        if (!h_over && cudaMallocHost(&h_over, 8) != cudaSuccess) {
+        if (!h_over && cudaMallocHost(&h_over, 16) != cudaSuccess) {
             set_err("cudaMallocHost", cudaGetLastError());
             return -6;
         }
         cudaMemcpyAsync(h_over, p.ctr + 6, 8, cudaMemcpyDeviceToHost, cs);
+        cudaMemcpyAsync(h_over + 1, q.chunk_abort, 8, cudaMemcpyDeviceToHost, cs);
         cudaError_t e = cudaStreamSynchronize(cs);
         if (e != cudaSuccess) {
             set_err("rtgpu_analyze_host", e);
             return -8;
         }
-        if (*h_over > 0) {
-            Dims full;
-            scan_dims_host((const i64 *)blobs, (const i64 *)set_off, n_sets, &full);
-            KParams r = p;
-            r.dims = full;
-            r.esc[0] = p.esc[2];
-            cudaMemcpyAsync(p.ctr + 4, p.ctr + 6, 8, cudaMemcpyDeviceToDevice, cs); /* list length */
-            cudaMemsetAsync(p.ctr + 1, 0, 8 * 2, cs);                             /* work counters */
-            cudaMemsetAsync(p.ctr + 5, 0, 8 * 3, cs); /* later lists, stage-1a counter */
-            r.esc[1] = p.esc[1];
-            r.esc[2] = p.esc[0]; /* free now */
-            rc = launch_general(r, cs);
-            if (rc) return rc;
+        if (h_over[1] == epoch) {
+            /* a chunk never arrived while the kernel waited (kernels
+             * serialised behind a profiler, a stalled copy engine): every
+             * copy has completed by now, so the batch re-runs unstreamed
+             * below and no set is left undecided */
+            cudaStreamSynchronize(cp);
+        } else {
+            if (*h_over > 0) {
+                Dims full;
+                scan_dims_host((const i64 *)blobs, (const i64 *)set_off, n_sets, &full);
+                KParams r = p;
+                r.dims = full;
+                r.esc[0] = p.esc[2];
+                cudaMemcpyAsync(p.ctr + 4, p.ctr + 6, 8, cudaMemcpyDeviceToDevice, cs); /* list length */
+                cudaMemsetAsync(p.ctr + 1, 0, 8 * 2, cs);                             /* work counters */
+                cudaMemsetAsync(p.ctr + 5, 0, 8 * 3, cs); /* later lists, stage-1a counter */
+                r.esc[1] = p.esc[1];
+                r.esc[2] = p.esc[0]; /* free now */
+                rc = launch_general(r, cs);
+                if (rc) return rc;
+            }
+            cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, cs);
+            cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, cs);
+            cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, cs);
+            e = cudaStreamSynchronize(cs);
+            if (e != cudaSuccess) {
+                set_err("rtgpu_analyze_host", e);
+                return -8;
+            }
+            return 0;
         }
-        cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, cs);
-        cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, cs);
-        cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, cs);
-        e = cudaStreamSynchronize(cs);
-        if (e != cudaSuccess) {
-            set_err("rtgpu_analyze_host", e);
-            return -8;
-        }
-        return 0;
     }
     const int chunks = (int)std::min<i64>(MAX_CHUNKS, std::max<i64>(1, n_sets / 4096));
     cudaStream_t cp = g_s_copy;

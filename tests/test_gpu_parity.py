@@ -219,3 +219,34 @@ def test_e2e_streamed_verdicts_mixed_dims():
     hv = np.concatenate([h.vsm[tb[s]:tb[s + 1]] for s in idx])
     sched = np.repeat(o["status"] == 1, ntask)
     assert np.array_equal(o["vsm"][sched], hv[sched])
+
+
+_NO_STREAM_CHILD = r"""
+import sys, numpy as np
+from fractions import Fraction
+from paper_2101_10463_b200 import _native
+from paper_2101_10463_b200.engine import analyze_packed
+gp = _native.gen_params_c(8, 5, (1000, 20000), (1000, 20000), (250, 5000), Fraction(1, 2), 0, 10,
+                          Fraction(12, 100), Fraction(1), compact=True)
+b = _native.generate(gp, [f"ns:{i}" for i in range(20000)])
+h = analyze_packed(*b, 0, 0)
+np.save(sys.argv[1], np.concatenate([h.status.astype(np.int64), h.vsm.astype(np.int64)]))
+"""
+
+
+@pytest.mark.gpu
+def test_e2e_no_stream_override_matches_streamed(tmp_path):
+    """RTGPU_NO_STREAM=1 (used for profiler runs, which serialise kernels)
+    switches the end-to-end verdict path to per-chunk launches; verdicts and
+    allocations are identical to the streamed path's."""
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for env_val in ("0", "1"):
+        f = tmp_path / f"o{env_val}.npy"
+        env = dict(os.environ, RTGPU_NO_STREAM=env_val)
+        subprocess.run([sys.executable, "-c", _NO_STREAM_CHILD, str(f)], check=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
