@@ -2,12 +2,15 @@
 verdict kernel waits for chunk copies queued behind it, its bounded wait
 times out, the abort word stops every warp, and the host re-runs the batch
 unstreamed.  Verdicts and allocations must still equal the device path's."""
+import os
+import sys
 import time
 
 import numpy as np
 from fractions import Fraction
 
-from paper_2101_10463_b200 import _native
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2101_10463_b200 import _native  # noqa: E402
 from paper_2101_10463_b200.engine import DeviceBatch, analyze_packed
 
 gp = _native.gen_params_c(8, 5, (1000, 20000), (1000, 20000), (250, 5000), Fraction(1, 2), 0, 10,
