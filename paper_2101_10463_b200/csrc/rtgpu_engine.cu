@@ -413,7 +413,14 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         *h_epoch = ++epoch;
         unsigned long long *flags_d = p.ctr + 8 + MAX_CHUNKS;
         cudaStream_t cs = g_s_comp[0], cp = g_s_copy;
-        cudaMemsetAsync(p.ctr, 0, 8 * 8, cs); /* stage counters, before the kernel */
+        /* stage counters, arrival flags and the abort word, zeroed before the
+         * kernel starts and before the copy stream writes any flag: a flag
+         * word can then hold only 0, a past epoch or this call's epoch --
+         * never leftover bytes of a freshly (re)allocated scratch buffer
+         * that happen to equal the epoch */
+        cudaMemsetAsync(p.ctr, 0, CTR_WORDS * 8, cs);
+        cudaEventRecord(g_ev_comp[1], cs);
+        cudaStreamWaitEvent(cp, g_ev_comp[1], 0);
         cudaMemcpyAsync(g_h_off.p, set_off, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
         cudaMemcpyAsync(g_h_tb.p, task_base, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
         auto enqueue_chunk = [&](int c) {
@@ -431,7 +438,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         q.n_sets = n_sets;
         q.wctr0 = &p.ctr[0];
         q.chunk_flag = flags_d;
-        q.chunk_abort = p.ctr + 8 + 2 * MAX_CHUNKS; /* epoch-valued: no reset needed */
+        q.chunk_abort = p.ctr + 8 + 2 * MAX_CHUNKS;
         q.epoch = epoch;
         q.chunks = chunks;
         /* the first chunk, then the kernel, then the rest: the kernel starts
