@@ -19,6 +19,77 @@ from .model import ExecBounds
 ZERO = Fraction(0)
 
 
+# ---------------------------------------------------------------- GPU path
+
+def _rows(tasks: Sequence[SuspTask], S: int) -> list[dict]:
+    """SuspTasks as engine rows: a two-copy task whose even copies carry the
+    suspension bounds and whose kernels have zero length (so the CPU chain's
+    gaps are exactly the suspension lower bounds)."""
+    rows = []
+    for i, t in enumerate(tasks):
+        m = t.m
+        ml_lo, ml_hi = [], []
+        for s in t.susp_segments:
+            ml_lo += [Q.ticks(s.lo, S), 0]
+            ml_hi += [Q.ticks(s.hi, S), 0]
+        rows.append({"m": m, "p": 2 * m - 2, "D": Q.ticks(t.deadline, S),
+                     "T": Q.ticks(t.period, S), "prio": i + 1, "idx": i,
+                     "cl_lo": [Q.ticks(b.lo, S) for b in t.exec_segments],
+                     "cl_hi": [Q.ticks(b.hi, S) for b in t.exec_segments],
+                     "ml_lo": ml_lo, "ml_hi": ml_hi, "gw_lo": [0] * (m - 1),
+                     "gw_hi": [0] * (m - 1), "gl": [0] * (m - 1), "an": [1] * (m - 1)})
+    return rows
+
+
+def _scale(tasks: Sequence[SuspTask], *extra) -> int:
+    vals = list(extra)
+    for t in tasks:
+        vals += [t.deadline, t.period]
+        for b in t.exec_segments + t.susp_segments:
+            vals += [b.lo, b.hi]
+    return Q.lcm_denominators(vals)
+
+
+def _query(tasks: Sequence[SuspTask], kind: int, index: int, horizon=ZERO, blocking=ZERO):
+    S = _scale(tasks, horizon, blocking)
+    blob = Q.build_blob(_rows(tasks, S), 1, 0, 1)
+    (st, num, den), = Q.run([blob], [(0, kind, len(tasks) - 1, index,
+                                      Q.ticks(max(horizon, ZERO), S), Q.ticks(blocking, S))])
+    return Q.value(st, num, den, S)
+
+
+def workload(t: SuspTask, h: int, horizon: Fraction) -> Fraction:
+    """W_t^h(horizon), Lemma 1 (suspension.py:107), on the GPU."""
+    if not 0 <= h < t.m:
+        raise ValueError(f"start segment {h} out of range")
+    if horizon <= 0:
+        return ZERO
+    return _query([t], Q.Q_WORKLOAD, h, Fraction(horizon))
+
+
+def max_workload(t: SuspTask, horizon: Fraction) -> Fraction:
+    """max over start segments (suspension.py:116), on the GPU."""
+    if horizon <= 0:
+        return ZERO
+    return _query([t], Q.Q_MAX_WORKLOAD, 0, Fraction(horizon))
+
+
+def segment_response(k: SuspTask, j: int, hp: Sequence[SuspTask],
+                     blocking: Fraction = ZERO) -> Optional[Fraction]:
+    """Lemma 2 recurrence for segment j of k (suspension.py:140), on the GPU."""
+    if not 0 <= j < k.m:
+        raise IndexError("segment index out of range")
+    return _query(list(hp) + [k], Q.Q_SEGMENT_RESPONSE, j, ZERO, Fraction(blocking))
+
+
+def task_response(k: SuspTask, hp: Sequence[SuspTask],
+                  blocking: Fraction = ZERO) -> Optional[Fraction]:
+    """Lemma 3: min(R1, R2) or None (suspension.py:155), on the GPU."""
+    return _query(list(hp) + [k], Q.Q_TASK_RESPONSE, 0, ZERO, Fraction(blocking))
+
+
+# ---------------------------------------------------------------- task model, host helpers
+
 @dataclass(frozen=True)
 class SuspTask:
     """m execution segments, m-1 suspensions, deadline and period
@@ -99,72 +170,3 @@ def fixed_point(base: Fraction, interference: Callable[[Fraction], Fraction],
         if nxt > bound:
             return None
         r = nxt
-
-
-# ---------------------------------------------------------------- GPU path
-
-def _rows(tasks: Sequence[SuspTask], S: int) -> list[dict]:
-    """SuspTasks as engine rows: a two-copy task whose even copies carry the
-    suspension bounds and whose kernels have zero length (so the CPU chain's
-    gaps are exactly the suspension lower bounds)."""
-    rows = []
-    for i, t in enumerate(tasks):
-        m = t.m
-        ml_lo, ml_hi = [], []
-        for s in t.susp_segments:
-            ml_lo += [Q.ticks(s.lo, S), 0]
-            ml_hi += [Q.ticks(s.hi, S), 0]
-        rows.append({"m": m, "p": 2 * m - 2, "D": Q.ticks(t.deadline, S),
-                     "T": Q.ticks(t.period, S), "prio": i + 1, "idx": i,
-                     "cl_lo": [Q.ticks(b.lo, S) for b in t.exec_segments],
-                     "cl_hi": [Q.ticks(b.hi, S) for b in t.exec_segments],
-                     "ml_lo": ml_lo, "ml_hi": ml_hi, "gw_lo": [0] * (m - 1),
-                     "gw_hi": [0] * (m - 1), "gl": [0] * (m - 1), "an": [1] * (m - 1)})
-    return rows
-
-
-def _scale(tasks: Sequence[SuspTask], *extra) -> int:
-    vals = list(extra)
-    for t in tasks:
-        vals += [t.deadline, t.period]
-        for b in t.exec_segments + t.susp_segments:
-            vals += [b.lo, b.hi]
-    return Q.lcm_denominators(vals)
-
-
-def _query(tasks: Sequence[SuspTask], kind: int, index: int, horizon=ZERO, blocking=ZERO):
-    S = _scale(tasks, horizon, blocking)
-    blob = Q.build_blob(_rows(tasks, S), 1, 0, 1)
-    (st, num, den), = Q.run([blob], [(0, kind, len(tasks) - 1, index,
-                                      Q.ticks(max(horizon, ZERO), S), Q.ticks(blocking, S))])
-    return Q.value(st, num, den, S)
-
-
-def workload(t: SuspTask, h: int, horizon: Fraction) -> Fraction:
-    """W_t^h(horizon), Lemma 1 (suspension.py:107), on the GPU."""
-    if not 0 <= h < t.m:
-        raise ValueError(f"start segment {h} out of range")
-    if horizon <= 0:
-        return ZERO
-    return _query([t], Q.Q_WORKLOAD, h, Fraction(horizon))
-
-
-def max_workload(t: SuspTask, horizon: Fraction) -> Fraction:
-    """max over start segments (suspension.py:116), on the GPU."""
-    if horizon <= 0:
-        return ZERO
-    return _query([t], Q.Q_MAX_WORKLOAD, 0, Fraction(horizon))
-
-
-def segment_response(k: SuspTask, j: int, hp: Sequence[SuspTask],
-                     blocking: Fraction = ZERO) -> Optional[Fraction]:
-    """Lemma 2 recurrence for segment j of k (suspension.py:140), on the GPU."""
-    if not 0 <= j < k.m:
-        raise IndexError("segment index out of range")
-    return _query(list(hp) + [k], Q.Q_SEGMENT_RESPONSE, j, ZERO, Fraction(blocking))
-
-
-def task_response(k: SuspTask, hp: Sequence[SuspTask],
-                  blocking: Fraction = ZERO) -> Optional[Fraction]:
-    """Lemma 3: min(R1, R2) or None (suspension.py:155), on the GPU."""
-    return _query(list(hp) + [k], Q.Q_TASK_RESPONSE, 0, ZERO, Fraction(blocking))
