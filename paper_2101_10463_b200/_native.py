@@ -152,6 +152,9 @@ def gen_params_c(n_tasks, n_subtasks, cpu_range, gpu_range, mem_range, util, mem
     """compact: int32 segment areas (header word 7 = 1); not for detail runs."""
     from fractions import Fraction
     u, e, lf = Fraction(util), Fraction(eps), Fraction(lo_frac)
+    for name, f in (("utilization", u), ("launch_overhead_frac", e), ("lo_frac", lf)):
+        if not (-2**63 < f.numerator < 2**63 and 0 < f.denominator < 2**63):
+            raise ValueError(f"{name} {f} does not fit the generator's int64 fraction")
     return GenParamsC(n_tasks, n_subtasks, cpu_range[0], cpu_range[1], gpu_range[0], gpu_range[1],
                       mem_range[0], mem_range[1], u.numerator, u.denominator, mem_model_code,
                       physical_sms, e.numerator, e.denominator, lf.numerator, lf.denominator,
@@ -177,6 +180,8 @@ def generate(params: GenParamsC, seeds, n_threads: int = 0):
     rc = L.rtgpu_generate(ctypes.byref(params), S, _ptr(int_seeds, ctypes.c_int64),
                           str_arr, n_threads, _ptr(blobs, ctypes.c_int64),
                           _ptr(set_off, ctypes.c_int64), _ptr(task_base, ctypes.c_int64))
+    if rc == -2:
+        raise ValueError("a generated deadline exceeds int64 (utilization too small)")
     if rc != 0:
         raise ValueError("invalid generator parameters")
     return blobs, set_off, task_base

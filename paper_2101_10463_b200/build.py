@@ -15,9 +15,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librtgpu.so")
-SOURCES = ["rtgpu_engine.cu", "rtgpu_k_f64.cu", "rtgpu_k_i64.cu", "rtgpu_k_i128.cu",
+SOURCES = ["rtgpu_engine.cu", "rtgpu_k_f64.cu", "rtgpu_k_i64.cu", "rtgpu_k_i128.cu", "rtgpu_k_lat.cu",
            "taskgen.cpp", "executor.cu", "simulator.cu"]
-HEADERS = ["engine_core.cuh", "kernel.cuh"]
+HEADERS = ["engine_core.cuh", "kernel.cuh", "lattice.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -49,6 +49,7 @@ struct KParams {
     int chunks = 1;
     i64 set_base;              /* front stage: first set of this launch (chunked e2e path) */
     unsigned long long *wctr0; /* front stage: this launch's work counter */
+    unsigned long long *lat_ctr = nullptr; /* lattice list stage's work counter */
 };
 
 /* minimum resident CTAs per SM the register allocation must allow */
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(256, MinBlocks<V>::value) fast_list_kernel(KPa
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if ((i64)idx >= count) break;
         const i64 s = p.esc[0][idx];
+        if (s < 0) continue; /* decided by the lattice stage */
         c.blob = p.blobs + p.set_off[s];
         const i64 tb = p.task_base[s];
         const int st = fast_verdict(tm, c, p.vsm + tb);
@@ -524,5 +526,7 @@ int launch_stage_f64(const KParams &p, int stage, cudaStream_t st);
 int launch_stage_i64(const KParams &p, int stage, cudaStream_t st);
 int launch_fast_list_i64(const KParams &p, cudaStream_t st);
 int launch_stage_i128(const KParams &p, int stage, cudaStream_t st);
+int launch_lattice_front(const KParams &p, cudaStream_t st);
+int launch_lattice_list(const KParams &p, cudaStream_t st);
 
 }  // namespace rtgpu

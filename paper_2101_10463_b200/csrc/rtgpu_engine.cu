@@ -61,7 +61,9 @@ DevBuf g_scratch; /* counters + escalation lists */
 const int MAX_CHUNKS = 32;
 /* [0..7] stage counters, [8, 8 + MAX_CHUNKS) per-chunk work counters,
  * [8 + MAX_CHUNKS, 8 + 2 MAX_CHUNKS) chunk arrival flags (streamed path) */
-const size_t CTR_WORDS = 9 + 2 * MAX_CHUNKS; /* [8+2*MAX_CHUNKS]: stream abort word */
+/* [8+2*MAX_CHUNKS]: stream abort word, [9+2*MAX_CHUNKS]: lattice list stage's work counter */
+const size_t CTR_WORDS = 10 + 2 * MAX_CHUNKS;
+const size_t LAT_CTR = 9 + 2 * MAX_CHUNKS;
 cudaStream_t g_s_copy = nullptr, g_s_comp[2] = {nullptr, nullptr};
 cudaEvent_t g_ev_chunk[MAX_CHUNKS], g_ev_comp[2];
 bool g_pipe_init = false;
@@ -118,11 +120,32 @@ int scan_dims_host(const i64 *blobs, const i64 *set_off, i64 n_sets, Dims *d) {
 #ifndef RTGPU_VERDICT_I64_FIRST
 #define RTGPU_VERDICT_I64_FIRST 1
 #endif
+/* RTGPU_NO_LATTICE=1 turns the lattice path off (A/B runs): every set the
+ * fast kernel hands on then takes the general stages */
+bool lattice_on() {
+    static const bool on = [] {
+        const char *v = getenv("RTGPU_NO_LATTICE");
+        return !(v && v[0] == '1');
+    }();
+    return on;
+}
+
+/* Stage 0: the fast kernel (verdict runs), the lattice kernel (RTGPU
+ * end-to-end bounds), else the general path in FP64. */
+int launch_front_any(const KParams &p, cudaStream_t st) {
+    if (lattice_on() && p.method == RTGPU_METHOD_RTGPU && p.flags == RTGPU_F_BOUNDS)
+        return launch_lattice_front(p, st);
+    return launch_front_f64(p, st);
+}
+
 int launch_general(KParams &p, cudaStream_t st) {
     int rc = 0;
     if (RTGPU_VERDICT_I64_FIRST && p.use_fast && !(p.flags & (RTGPU_F_FIRST_I64 | RTGPU_F_FIRST_I128))) {
         p.last_stage = 2;
-        rc = launch_fast_list_i64(p, st); /* stage 1a: range escalations in int64 */
+        /* stage 1L: the lattice path over the fast kernel's escalations (wide
+         * platforms whose fixed scale does not fit FP64) */
+        if (lattice_on()) rc = launch_lattice_list(p, st);
+        if (!rc) rc = launch_fast_list_i64(p, st); /* stage 1a: range escalations in int64 */
         if (!rc) rc = launch_stage_i64(p, 1, st);
         if (g_timing) cudaEventRecord(g_ev[2], st);
         if (!rc) rc = launch_stage_i128(p, 2, st);
@@ -175,6 +198,7 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     p.esc[2] = p.esc[1] + n_sets;
     p.set_base = 0;
     p.wctr0 = &p.ctr[0];
+    p.lat_ctr = &p.ctr[LAT_CTR];
     p.use_fast = flags == 0 && method == RTGPU_METHOD_RTGPU;
     cudaError_t e = cudaMemsetAsync(p.ctr, 0, CTR_WORDS * sizeof(unsigned long long), st);
     if (e != cudaSuccess) {
@@ -186,7 +210,7 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
         g_ev_init = true;
     }
     if (g_timing) cudaEventRecord(g_ev[0], st);
-    int rc = launch_front_f64(p, st);
+    int rc = launch_front_any(p, st);
     if (g_timing) cudaEventRecord(g_ev[1], st);
     rc = rc ? rc : launch_general(p, st);
     g_ev_valid = g_timing && !rc;
@@ -389,6 +413,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
     p.esc[0] = (i64 *)((char *)g_scratch.p + CTR_WORDS * 8);
     p.esc[1] = p.esc[0] + n_sets;
     p.esc[2] = p.esc[1] + n_sets;
+    p.lat_ctr = &p.ctr[LAT_CTR];
     p.use_fast = flags == 0 && method == RTGPU_METHOD_RTGPU;
     /* RTGPU_NO_STREAM=1 forces the chunked-launch path: under a profiler that
      * serialises kernels (ncu) the persistent streamed kernel would wait for
@@ -485,6 +510,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
                 cudaMemcpyAsync(p.ctr + 4, p.ctr + 6, 8, cudaMemcpyDeviceToDevice, cs); /* list length */
                 cudaMemsetAsync(p.ctr + 1, 0, 8 * 2, cs);                             /* work counters */
                 cudaMemsetAsync(p.ctr + 5, 0, 8 * 3, cs); /* later lists, stage-1a counter */
+                cudaMemsetAsync(p.ctr + LAT_CTR, 0, 8, cs); /* lattice list counter */
                 r.esc[1] = p.esc[1];
                 r.esc[2] = p.esc[0]; /* free now */
                 rc = launch_general(r, cs);
@@ -518,7 +544,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         q.set_base = a;
         q.n_sets = b - a;
         q.wctr0 = &p.ctr[8 + c];
-        rc = launch_front_f64(q, cs);
+        rc = launch_front_any(q, cs);
     }
     if (rc) return rc;
     /* escalation stages and results on compute stream 0 after every chunk */

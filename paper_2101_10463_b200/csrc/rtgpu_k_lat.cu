@@ -1,0 +1,111 @@
+/* rtgpu_k_lat.cu -- the lattice path's kernel (lattice.cuh): exact FP64
+ * verdicts and end-to-end bounds with per-task scales, for any SM count. */
+#include "kernel.cuh"
+#include "lattice.cuh"
+
+namespace rtgpu {
+
+/* Persistent teams of W warps, one task set each (256 threads per CTA, 8 / W
+ * teams, team t on named barrier t + 1).  LIST = false: the sets
+ * [set_base, set_base + n_sets) (the front stage of bounds runs); LIST =
+ * true: the sets the fast kernel handed on in esc[0] (verdict runs), whose
+ * decided entries become -1.  Sets the path does not take go on to esc[0]
+ * (front) or stay in it (list) for the general stages. */
+template <int W, bool LIST>
+__global__ void __launch_bounds__(256, 4) lattice_kernel(KParams p, int slab_bytes) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int team = warp / W;
+    LTeam<W> tm{lane, warp % W, team + 1};
+    LCtx c;
+    c.hbase = nullptr;
+    c.base = team * slab_bytes;
+    c.L.init(p.dims);
+    const bool bounds = (p.flags & RTGPU_F_BOUNDS) != 0;
+    const i64 count = LIST ? (i64)p.ctr[4] : p.n_sets;
+    unsigned long long *wctr = LIST ? p.lat_ctr : p.wctr0;
+    i64 *slot = (i64 *)(rt_dyn_smem + c.base + c.L.o_red) + 16; /* the team's set index */
+    for (;;) {
+        if (tm.leader()) *slot = (i64)atomicAdd(wctr, 1ull);
+        tm.sync();
+        const i64 idx = *slot;
+        tm.sync();
+        if (idx >= count) break;
+        const i64 s = LIST ? p.esc[0][idx] : p.set_base + idx;
+        if (s < 0) continue;
+        c.blob = p.blobs + p.set_off[s];
+        const i64 tb = p.task_base[s];
+        i64 evals = 0;
+        const int st = lattice_set(tm, c, bounds, p.vsm + tb, bounds ? p.e2e + tb : nullptr,
+                                   bounds ? p.den + tb : nullptr, evals);
+        if (st == ST_ESCALATE) {
+            if (!LIST && tm.leader()) {
+                unsigned long long pos = atomicAdd(&p.ctr[4], 1ull);
+                p.esc[0][pos] = s;
+            }
+            tm.sync();
+            continue;
+        }
+        if (tm.leader()) {
+            p.status[s] = st;
+            p.evals[s] = evals;
+            if (LIST) p.esc[0][idx] = -1;
+        }
+        tm.sync();
+    }
+}
+
+/* team width: the fewest warps per set that keep ~32 warps resident per SM
+ * (the register budget at 64 registers) within 227 KB of shared memory */
+static int lat_width(const LSlab &L) {
+    if (L.bytes * 32 <= 220 * 1024) return 1;
+    if (L.bytes * 16 <= 220 * 1024) return 2;
+    return 4;
+}
+
+template <int W, bool LIST> static void *lat_kernel_ptr() { return (void *)lattice_kernel<W, LIST>; }
+
+static int lat_launch(const KParams &p, bool list, cudaStream_t st) {
+    LSlab L;
+    L.init(p.dims);
+    const int W = lat_width(L);
+    const int teams = 8 / W;
+    const int bytes = L.bytes * teams;
+    if (bytes > 227 * 1024) {
+        set_err_msg("task sets too large for shared memory");
+        return -3;
+    }
+    void *k = W == 1 ? (list ? lat_kernel_ptr<1, true>() : lat_kernel_ptr<1, false>())
+            : W == 2 ? (list ? lat_kernel_ptr<2, true>() : lat_kernel_ptr<2, false>())
+                     : (list ? lat_kernel_ptr<4, true>() : lat_kernel_ptr<4, false>());
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) {
+        set_err("cudaFuncSetAttribute", e);
+        return -4;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, bytes);
+    if (per_sm < 1) per_sm = 1;
+    i64 grid = (i64)sms * per_sm;
+    if (!list) {
+        const i64 want = (p.n_sets + teams - 1) / teams;
+        if (want < grid) grid = want;
+    }
+    if (grid < 1) grid = 1;
+    int sb = L.bytes;
+    void *args[] = {(void *)&p, (void *)&sb};
+    e = cudaLaunchKernel(k, dim3((unsigned)grid), dim3(256), args, bytes, st);
+    count_launch();
+    if (e != cudaSuccess) {
+        set_err("lattice_kernel launch", e);
+        return -5;
+    }
+    return 0;
+}
+
+int launch_lattice_front(const KParams &p, cudaStream_t st) { return lat_launch(p, false, st); }
+int launch_lattice_list(const KParams &p, cudaStream_t st) { return lat_launch(p, true, st); }
+
+}  // namespace rtgpu

@@ -30,6 +30,30 @@
 namespace {
 
 typedef unsigned __int128 u128;
+
+/* floor(a * b / d) for a * b up to 2^256 (d > 0, quotient < 2^127): the
+ * deadline formula with a utilisation given as a binary fraction (Fraction
+ * of a float has a 2^55 denominator) exceeds 128 bits.  Schoolbook
+ * 256-bit product, then restoring division one bit at a time -- only on
+ * the overflow path. */
+u128 muldiv_u256(u128 a, u128 b, u128 d) {
+    const uint64_t a0 = (uint64_t)a, a1 = (uint64_t)(a >> 64), b0 = (uint64_t)b, b1 = (uint64_t)(b >> 64);
+    const u128 p00 = (u128)a0 * b0, p01 = (u128)a0 * b1, p10 = (u128)a1 * b0, p11 = (u128)a1 * b1;
+    u128 mid = (p00 >> 64) + (uint64_t)p01 + (uint64_t)p10;
+    u128 lo = ((u128)(uint64_t)mid << 64) | (uint64_t)p00;
+    u128 hi = p11 + (p01 >> 64) + (p10 >> 64) + (mid >> 64);
+    u128 rem = 0, q = 0;
+    for (int bit = 255; bit >= 0; bit--) {
+        const bool top = (rem >> 127) != 0;
+        rem = (rem << 1) | (u128)((bit >= 128 ? (hi >> (bit - 128)) : (lo >> bit)) & 1);
+        q <<= 1;
+        if (top || rem >= d) {
+            rem -= d;
+            q |= 1;
+        }
+    }
+    return q;
+}
 typedef __int128 i128;
 
 /* ------------------------------------------------------------ SHA-512 */
@@ -226,7 +250,8 @@ int64_t lo_of(int64_t hi, const rtgpu_gen_params *p) {
 }
 
 /* workbench.py:101 generate_taskset for one seed, written as a blob. */
-void gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
+/* false: a deadline does not fit int64 (parameters out of range) */
+bool gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
     const int n = p->n_tasks, m = p->n_subtasks;
     std::vector<uint64_t> raw(n);
     for (;;) {
@@ -272,9 +297,12 @@ void gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
         for (int64_t v : d.ml_hi) demand += v;
         for (int64_t v : d.gw_hi) demand += v;
         /* D = max(1, floor(demand / (raw_i * U / total))) */
-        u128 num = (u128)demand * total * (u128)p->util_den;
-        u128 den = (u128)raw[i] * (u128)p->util_num;
-        u128 q = num / den;
+        const u128 den = (u128)raw[i] * (u128)p->util_num; /* < 2^117 */
+        const u128 dt = (u128)demand * total;              /* < 2^103 */
+        u128 num, q;
+        if (__builtin_mul_overflow(dt, (u128)p->util_den, &num)) q = muldiv_u256(dt, (u128)p->util_den, den);
+        else q = num / den;
+        if (q > (u128)INT64_MAX) return false; /* a deadline beyond int64 */
         d.D = q < 1 ? 1 : (int64_t)q;
     }
     std::vector<int> order(n);
@@ -348,6 +376,7 @@ void gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
         }
         seg += (int64_t)v.size();
     }
+    return true;
 }
 
 }  // namespace
@@ -379,16 +408,19 @@ int rtgpu_generate(const rtgpu_gen_params *p, int64_t n_sets, const int64_t *int
     }
     if (n_threads < 1) n_threads = 1;
     std::vector<std::thread> th;
+    std::vector<char> bad(n_threads, 0);
     for (int t = 0; t < n_threads; t++)
-        th.emplace_back([=]() {
+        th.emplace_back([=, &bad]() {
             MT g;
             for (int64_t s = t; s < n_sets; s += n_threads) {
                 if (str_seeds) seed_str(g, str_seeds[s]);
                 else seed_int(g, int_seeds[s]);
-                gen_one(p, g, blobs + s * words);
+                if (!gen_one(p, g, blobs + s * words)) bad[t] = 1;
             }
         });
     for (auto &x : th) x.join();
+    for (char b : bad)
+        if (b) return -2; /* a deadline beyond int64 */
     return 0;
 }
 

@@ -212,7 +212,11 @@ def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = MARG
 
 
 def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = True,
-              cpu_mode: int = CPU_PARALLEL, bus_mode: int = BUS_FP):
+              cpu_mode: int = CPU_PARALLEL, bus_mode: int = BUS_FP, priorities=None):
+    """Run the tasks on their SM partitions.  priorities[i] is task i's fixed
+    priority (smaller = higher, as TaskSpec.priority): the bus arbiter and the
+    CPU ranks use it, so it must be the priority the analysis assumed
+    (default: the order of defs)."""
     L = _lib()
     if L.rtgpu_exec_configure(cpu_mode, bus_mode):
         raise ValueError(L.rtgpu_exec_last_error().decode())
@@ -231,7 +235,7 @@ def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = 
         for j, v in enumerate(d.kernel_items):
             t.kernel_items[j] = int(v)
         t.kernel_iters = iters
-        t.priority = i + 1
+        t.priority = int(priorities[i]) if priorities is not None else i + 1
         mk = mask_of(sms)
         for w in range(MASK_WORDS):
             t.sm_mask[w] = mk[w]
@@ -322,7 +326,10 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
     if nxt > n_sm:
         raise ValueError(f"partitions need {nxt} SMs, the GPU has {n_sm}")
     out.allocation = {s.id: alloc[s.id] for s in specs}
-    res = run_tasks(defs, parts, iters, horizon_us, cpu_mode=cpu_mode, bus_mode=bus_mode)
+    # the executor arbitrates the bus and the CPU with the analysis' own
+    # (deadline-monotonic) priorities, not the order tasks were drawn in
+    res = run_tasks(defs, parts, iters, horizon_us, cpu_mode=cpu_mode, bus_mode=bus_mode,
+                    priorities=[s.priority for s in specs])
     out.cpu_mode, out.bus_mode = int(res[0].cpu_mode), int(res[0].bus_mode)
     ratios, kok = [], True
     for s, d, r, sms in zip(specs, defs, res, parts):

@@ -14,6 +14,25 @@
 #include <vector>
 
 #include "../../paper_2101_10463_b200/csrc/engine_core.cuh"
+#include "../../paper_2101_10463_b200/csrc/lattice.cuh"
+
+#ifdef RT_COUNTERS
+namespace rtgpu {
+long long g_cnt_interf[2], g_cnt_lfp[2], g_cnt_eval, g_cnt_views, g_cnt_rounds;
+long long g_cnt_flfp[8], g_cnt_fit[8], g_cnt_frounds, g_cnt_passes;
+}
+extern "C" void host_counters(long long *out, int reset) {
+    using namespace rtgpu;
+    long long v[] = {g_cnt_interf[0], g_cnt_interf[1], g_cnt_lfp[0], g_cnt_lfp[1], g_cnt_eval, g_cnt_rounds,
+                     g_cnt_flfp[0], g_cnt_flfp[1], g_cnt_fit[0], g_cnt_fit[1], g_cnt_frounds, g_cnt_passes};
+    for (int i = 0; i < 12; i++) out[i] = v[i];
+    if (reset) {
+        g_cnt_interf[0] = g_cnt_interf[1] = g_cnt_lfp[0] = g_cnt_lfp[1] = g_cnt_eval = g_cnt_rounds = 0;
+        for (int i = 0; i < 8; i++) g_cnt_flfp[i] = g_cnt_fit[i] = 0;
+        g_cnt_frounds = g_cnt_passes = 0;
+    }
+}
+#endif
 
 using namespace rtgpu;
 
@@ -171,6 +190,38 @@ extern "C" int host_query(const int64_t *blobs, const int64_t *set_off, int64_t 
         }
         if (st == ST_ESCALATE) st = RTGPU_RANGE;
         status[qi] = st;
+    }
+    return 0;
+}
+
+/* The lattice path (lattice.cuh) alone: status ST_ESCALATE (99) where it
+ * hands the set on. */
+extern "C" int host_lattice_batch(const int64_t *blobs, const int64_t *set_off, const int64_t *task_base,
+                                  int64_t n_sets, int bounds, int32_t *status, int64_t *evals, int32_t *vsm,
+                                  int64_t *e2e, int64_t *den) {
+    Dims d;
+    d.maxn = 1;
+    d.MC = 1;
+    d.MP = 0;
+    for (int64_t s = 0; s < n_sets; s++) {
+        const int64_t *h = blobs + set_off[s];
+        if (h[0] > d.maxn) d.maxn = (int)h[0];
+        if (h[5] > d.MC) d.MC = (int)h[5];
+        if (h[6] > d.MP) d.MP = (int)h[6];
+    }
+    LCtx c;
+    c.L.init(d);
+    std::vector<unsigned char> slab((size_t)c.L.bytes + 64);
+    c.hbase = (unsigned char *)(((uintptr_t)slab.data() + 15) & ~(uintptr_t)15);
+    c.base = 0;
+    for (int64_t s = 0; s < n_sets; s++) {
+        c.blob = (const i64 *)blobs + set_off[s];
+        LSeq tm;
+        const int64_t tb = task_base[s];
+        i64 ev = 0;
+        status[s] = lattice_set(tm, c, bounds != 0, vsm + tb, bounds ? (i64 *)e2e + tb : nullptr,
+                                bounds ? (i64 *)den + tb : nullptr, ev);
+        evals[s] = ev;
     }
     return 0;
 }

@@ -11,12 +11,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 SRC = os.path.join(HERE, "engine_host.cpp")
 CORE = os.path.join(ROOT, "paper_2101_10463_b200", "csrc", "engine_core.cuh")
+LAT = os.path.join(ROOT, "paper_2101_10463_b200", "csrc", "lattice.cuh")
 LIB = os.path.join(HERE, "libenginehost.so")
 _lib = None
 
 
 def build():
-    newest = max(os.path.getmtime(SRC), os.path.getmtime(CORE))
+    newest = max(os.path.getmtime(SRC), os.path.getmtime(CORE), os.path.getmtime(LAT))
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", LIB, SRC],
                        check=True)
@@ -82,3 +83,22 @@ def query(sets, queries):
     L.host_query(_p(blobs, ctypes.c_int64), _p(set_off, ctypes.c_int64), len(sets), qa, n,
                  _p(st, ctypes.c_int32), _p(num, ctypes.c_int64), _p(den, ctypes.c_int64))
     return [(int(st[i]), int(num[i]), int(den[i])) for i in range(n)]
+
+
+def lattice_batch(blobs, set_off, task_base, bounds=False):
+    """The lattice path alone (status 99 = handed on to the general stages)."""
+    L = lib()
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    p32 = ctypes.POINTER(ctypes.c_int32)
+    L.host_lattice_batch.argtypes = [p64, p64, p64, ctypes.c_int64, ctypes.c_int, p32, p64, p32, p64, p64]
+    S = len(set_off) - 1
+    T = int(task_base[-1])
+    out = dict(status=np.zeros(S, np.int32), evals=np.zeros(S, np.int64), vsm=np.zeros(T, np.int32),
+               e2e_num=np.zeros(T, np.int64), den=np.ones(T, np.int64))
+    blobs = np.ascontiguousarray(blobs, np.int64)
+    L.host_lattice_batch(_p(blobs, ctypes.c_int64), _p(np.ascontiguousarray(set_off, np.int64), ctypes.c_int64),
+                         _p(np.ascontiguousarray(task_base, np.int64), ctypes.c_int64), S, int(bounds),
+                         _p(out["status"], ctypes.c_int32), _p(out["evals"], ctypes.c_int64),
+                         _p(out["vsm"], ctypes.c_int32), _p(out["e2e_num"], ctypes.c_int64),
+                         _p(out["den"], ctypes.c_int64))
+    return out

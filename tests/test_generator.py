@@ -35,3 +35,19 @@ def test_generator_threads_deterministic():
     a = _native.generate(gp, list(range(300)), n_threads=1)[0]
     b = _native.generate(gp, list(range(300)), n_threads=7)[0]
     assert np.array_equal(a, b)
+
+
+def test_generator_float_utilization_matches_reference():
+    """A float utilisation becomes Fraction(float) (a 2^55 denominator): the
+    deadline product then exceeds 128 bits and takes the 256-bit path.
+    Deadlines pinned to the reference generator (workbench.py:101) run
+    here with seed 7 (GenParams(n_tasks=16, n_subtasks=9,
+    target_utilization=0.1) and n_tasks=32, n_subtasks=5)."""
+    want = {16: [33573336, 82044774, 15606142], 32: [48175972, 104472749, 24214503]}
+    for n, m in ((16, 9), (32, 5)):
+        gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), Fraction(0.1), 0,
+                                  148, Fraction(12, 100), Fraction(1))
+        blobs, _, _ = _native.generate(gp, [7])
+        recs = blobs[8:8 + 8 * n].reshape(n, 8)
+        by_index = {int(r[6]): int(r[2]) for r in recs}
+        assert [by_index[i] for i in range(3)] == want[n]
