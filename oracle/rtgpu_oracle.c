@@ -736,6 +736,53 @@ static int greedy_rtgpu(octx *c, const oset *s, const int *mins, int *gn, aview 
 }
 
 #define ORACLE_GREEDY 0x100u
+#define ORACLE_PREFIX 0x200u
+
+/* Prefix-pruned enumeration (flags & ORACLE_PREFIX): the reference's
+ * lexicographic grid search (analysis.py:250 over gpu.py:43 _compositions),
+ * skipping only subtrees whose prefix already fails.  It rests on nothing
+ * but the prefix property visible in analysis.py:156-217 -- task k's bounds
+ * read the counts of higher-priority tasks only (interference from hp(k);
+ * the blocking term is lower-priority copy lengths, independent of the
+ * allocation) -- and NOT on the monotonicity / dominance argument the
+ * engine's greedy descent and ORACLE_GREEDY use.  Same first schedulable
+ * allocation as the full enumeration; the budget (task evaluations) makes
+ * undecidable sets RTGPU_UNDECIDED.  Returns 1 schedulable (gn holds the
+ * allocation), 0 unschedulable. */
+static int prefix_rtgpu(octx *c, const oset *s, const int *mins, const int *ids, int nid, int *gn, aview *av,
+                        trep *rep) {
+    int x[MAXT];
+    for (int k = 0; k < s->n; k++) gn[k] = s->t[k].g > 0 ? mins[k] : 0;
+    if (nid == 0) {
+        build_view(c, s, gn, av);
+        return eval_rtgpu(c, av, rep);
+    }
+    int q = 0;
+    x[0] = mins[ids[0]] - 1;
+    for (;;) {
+        /* next count of GPU task q within its range, else backtrack */
+        int64_t used = 0, after = 0;
+        for (int a = 0; a < q; a++) used += x[a];
+        for (int a = q + 1; a < nid; a++) after += mins[ids[a]];
+        if (x[q] + 1 > s->gn - used - after) {
+            gn[ids[q]] = mins[ids[q]];
+            if (--q < 0) return 0;
+            continue;
+        }
+        x[q]++;
+        gn[ids[q]] = x[q];
+        build_view(c, s, gn, av);
+        int ok = eval_rtgpu(c, av, rep);
+        if (ok) return 1;
+        /* first failing task; tasks before GPU task q + 1 depend on x[0..q] only */
+        int f = 0;
+        while (f < s->n && rep[f].present && rep[f].e2e != NONE128 && rep[f].e2e <= av->v[f].D) f++;
+        const int next_pos = q + 1 < nid ? ids[q + 1] : s->n;
+        if (f < next_pos) continue; /* this prefix fails for every completion */
+        q++;
+        x[q] = mins[ids[q]] - 1;
+    }
+}
 
 int oracle_analyze_set(const int64_t *blob, int method, unsigned flags, int64_t budget,
                        int32_t *status, int64_t *evals, int32_t *vsm, int64_t *e2e_num,
@@ -809,6 +856,30 @@ int oracle_analyze_set(const int64_t *blob, int method, unsigned flags, int64_t 
         }
         build_view(&c, &s, gn, &av);
         eval_rtgpu(&c, &av, rep);
+        write_report(&s, &av, rep, method, gn, ok, blob_detail, vsm, e2e_num, den, &range_err);
+        if (range_err) *status = RTGPU_RANGE;
+        return 0;
+    }
+    if ((flags & ORACLE_PREFIX) && method == RTGPU_METHOD_RTGPU) {
+        int64_t need = 0;
+        for (int q = 0; q < nid; q++) need += mins[ids[q]];
+        if (need > s.gn) goto unsched_empty;
+        int ok = prefix_rtgpu(&c, &s, mins, ids, nid, gn, &av, rep);
+        *status = ok ? RTGPU_SCHEDULABLE : RTGPU_UNSCHEDULABLE;
+        *evals = c.evals;
+        if (!ok) {
+            /* the reference reports the lexicographically last allocation */
+            int first = -1;
+            int64_t others = 0;
+            for (int q = 0; q < nid; q++) {
+                if (first < 0) first = ids[q];
+                else others += mins[ids[q]];
+            }
+            for (int k = 0; k < s.n; k++)
+                gn[k] = s.t[k].g > 0 ? (k == first ? (int)(s.gn - others) : mins[k]) : 0;
+            build_view(&c, &s, gn, &av);
+            eval_rtgpu(&c, &av, rep);
+        }
         write_report(&s, &av, rep, method, gn, ok, blob_detail, vsm, e2e_num, den, &range_err);
         if (range_err) *status = RTGPU_RANGE;
         return 0;

@@ -167,6 +167,15 @@ struct LCtx {
     RT_HD Seg32 segs(int i) const { return Seg32{(const int32_t *)blob + seg()[i]}; }
 };
 
+/* What a lane remembers of its walks between the iterations of one fixed
+ * point (same task, same start segments; the window only grows): the best
+ * walk ending inside a segment (m1, its remaining length r1), the best one
+ * ending in a gap (m0), and how far the window may grow with every walk
+ * exactly predictable (v: the least remaining length / gap).  Scale units. */
+struct LCache {
+    double m1, r1, m0, v, H;
+};
+
 /* ------------------------------------------------------------ teams */
 
 #ifdef __CUDACC__
@@ -179,6 +188,9 @@ template <int W> struct LTeam {
     }
     __device__ __forceinline__ bool leader() const { return lane == 0 && warp == 0; }
     __device__ __forceinline__ int width() const { return W; }
+    typedef LCache Cache; /* the lane's own */
+    __device__ __forceinline__ void cache_reset(Cache &c) const { c.H = -1; }
+    __device__ __forceinline__ Cache &cache_ptr(Cache &c) const { return c; }
     template <class F> __device__ __forceinline__ void pfor(int n, F f) const {
         #pragma unroll 1
         for (int i = warp * 32 + lane; i < n; i += 32 * W) f(i);
@@ -192,6 +204,13 @@ struct LSeq {
     RT_HD void sync() const {}
     RT_HD bool leader() const { return true; }
     RT_HD int width() const { return 1; }
+    struct Cache {
+        LCache c[32]; /* one per emulated lane */
+    };
+    RT_HD void cache_reset(Cache &c) const {
+        for (int i = 0; i < 32; i++) c.c[i].H = -1;
+    }
+    RT_HD LCache *cache_ptr(Cache &c) const { return c.c; }
     template <class F> RT_HD void pfor(int n, F f) const {
         for (int i = 0; i < n; i++) f(i);
     }
@@ -201,22 +220,26 @@ struct LSeq {
 
 /* W_i^h(H) of suspension.py:77 over a regular chain view at the task's
  * scale: P[0..p] (P[p] = cycle length C), EP[0..p], F1, 1/C; rho = the
- * remaining slope-1 length when the window ends inside a segment.  First
- * (partial) job, or a floor-division jump over whole cycles and the last
- * one; then the last segment start <= the window end by a galloping binary
- * search (half = power of two >= PM / 2). */
-RT_HD double walk_lat(const double *v, int PM, int half, int p, int h, double H, double &rho) {
+ * remaining slope-1 length when the window ends inside a segment, else
+ * gap = the distance from the window's end to the next segment start (the
+ * window can grow by that much with W unchanged).  First (partial) job, or
+ * a floor-division jump over whole cycles and the last one; then the last
+ * segment start <= the window end by a galloping binary search (half =
+ * power of two >= PM / 2). */
+RT_HD double walk_lat(const double *v, int PM, int half, int p, int h, double H, double &rho, double &gap) {
     rho = 0;
+    gap = 0;
     if (H <= 0) return 0;
     const double *P = v, *EP = v + PM + 1;
     const double lim = H + P[h];
     const double F1 = v[2 * PM + 2];
-    double w0, Hs;
+    double w0, Hs, nxt;
     int x;
     if (F1 > lim) {
         x = h;
         Hs = lim;
         w0 = -EP[h];
+        nxt = F1; /* after the first job's last segment: the second job */
     } else {
         const double C = P[p];
         double r;
@@ -224,6 +247,7 @@ RT_HD double walk_lat(const double *v, int PM, int half, int p, int h, double H,
         Hs = r;
         w0 = EP[p] - EP[h] + kq * EP[p];
         x = 0;
+        nxt = C; /* the next cycle's first segment */
     }
     #pragma unroll 1
     for (int st = half; st > 0; st >>= 1) {
@@ -236,8 +260,10 @@ RT_HD double walk_lat(const double *v, int PM, int half, int p, int h, double H,
         rho = e1 - e0 - tail;
         return w0 + e0 + tail;
     }
+    gap = (x < p - 1 ? P[x + 1] : nxt) - Hs;
     return w0 + e1;
 }
+
 
 /* per-iteration accumulators of the interference rounds */
 struct LatAcc {
@@ -318,7 +344,7 @@ RT_HD LChains lat_chains(const LCtx &c, int k, int res, int W) {
  * start segments h = slot % G, + G, ... and the slope-1 length (ticks) of a
  * maximising walk (largest among ties); s / invs / phv are the task's. */
 RT_HD void lat_slot(const LChains &ch, double bN, i64 bf, i64 d, double invd, int i0, int slot, double &bw,
-                    double &br, double &s, double &invs, double &phv) {
+                    double &br, double &s, double &invs, double &phv, LCache *cc) {
     const int G = 1 << ch.lg;
     const int i = i0 + (slot >> ch.lg), h0 = slot & (G - 1);
     bw = 0;
@@ -353,13 +379,53 @@ RT_HD void lat_slot(const LChains &ch, double bN, i64 bf, i64 d, double invd, in
     const int p = ch.res == K_CPU ? li_m(info) : li_p(info);
     const double *v = (const double *)(sb + ch.vbase) + (size_t)i * ch.stride;
     const double H = Hi + hf;
-    #pragma unroll 1
-    for (int h = h0; h < p; h += G) {
-        double r;
-        const double w = walk_lat(v, ch.PM, ch.half, p, h, H, r);
-        if (w > bw || (w == bw && r > br)) {
-            bw = w;
-            br = r;
+    const double NONE = -1e300;
+    if (cc && cc->H >= 0 && H - cc->H <= cc->v) {
+        /* every walk predictable: the ones inside a segment grew by the
+         * window's growth, the ones in a gap did not move (a walk that just
+         * reached a boundary keeps its exact value; its slope-1 length is
+         * under-reported as 0, which only shortens the jump) */
+        const double dl = H - cc->H;
+        cc->m1 += dl;
+        cc->r1 -= dl;
+        cc->v -= dl;
+        cc->H = H;
+        if (cc->m1 >= cc->m0) {
+            bw = cc->m1;
+            br = cc->r1;
+        } else {
+            bw = cc->m0;
+        }
+    } else {
+        double m1 = NONE, r1 = 0, m0 = 0, vmin = 1e300;
+        #pragma unroll 1
+        for (int h = h0; h < p; h += G) {
+            RT_COUNT(g_cnt_frounds);
+            double r, gp;
+            const double w = walk_lat(v, ch.PM, ch.half, p, h, H, r, gp);
+            if (r > 0) {
+                if (w > m1 || (w == m1 && r > r1)) {
+                    m1 = w;
+                    r1 = r;
+                }
+                vmin = tmin(vmin, r);
+            } else {
+                m0 = tmax(m0, w);
+                vmin = tmin(vmin, gp);
+            }
+        }
+        if (m1 >= m0) {
+            bw = m1;
+            br = r1;
+        } else {
+            bw = m0;
+        }
+        if (cc) {
+            cc->m1 = m1;
+            cc->r1 = r1;
+            cc->m0 = m0;
+            cc->v = vmin;
+            cc->H = H;
         }
     }
     br = br > 0 ? (br + hf - phv) * invs : 0.0;
@@ -369,14 +435,20 @@ RT_HD void lat_slot(const LChains &ch, double bN, i64 bf, i64 d, double invd, in
 #ifdef __CUDACC__
 template <int W>
 __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &ch, double bN, i64 bf, i64 d,
-                                             double invd) {
+                                             double invd, LCache &cache) {
     LatAcc a = {0.0, 0.0, 0.0, false};
     const int per = 32 >> ch.lg, G = 1 << ch.lg;
     const int R = (ch.k + per - 1) / per;
+#ifdef RTGPU_LAT_NOCACHE
+    LCache *cc = nullptr;
+    (void)cache;
+#else
+    LCache *cc = R <= W ? &cache : nullptr; /* one round per warp: the lane's walks are the same every iteration */
+#endif
     #pragma unroll 1
     for (int r = tm.warp; r < R; r += W) {
         double bw, br, s, invs, phv;
-        lat_slot(ch, bN, bf, d, invd, r * per, tm.lane, bw, br, s, invs, phv);
+        lat_slot(ch, bN, bf, d, invd, r * per, tm.lane, bw, br, s, invs, phv, cc);
         for (int off = 1; off < G; off <<= 1) {
             const double ow = shfl_x(bw, off), orr = shfl_x(br, off);
             if (ow > bw || (ow == bw && orr > br)) {
@@ -419,15 +491,20 @@ __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &
 }
 #endif
 
-RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 d, double invd) {
+RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 d, double invd, LCache *cache) {
     LatAcc a = {0.0, 0.0, 0.0, false};
     const int per = 32 >> ch.lg, G = 1 << ch.lg;
+#ifdef RTGPU_LAT_NOCACHE
+    const bool one = false;
+#else
+    const bool one = ch.k <= per; /* one round: the emulated lanes keep their caches */
+#endif
     for (int i0 = 0; i0 < ch.k; i0 += per)
         for (int g0 = 0; g0 < 32; g0 += G) {
             double m = 0, rm = 0, s = 1, invs = 1, phv = 0;
             for (int x = 0; x < G; x++) {
                 double bw, br;
-                lat_slot(ch, bN, bf, d, invd, i0, g0 + x, bw, br, s, invs, phv);
+                lat_slot(ch, bN, bf, d, invd, i0, g0 + x, bw, br, s, invs, phv, one ? cache + g0 + x : nullptr);
                 if (x == 0 || bw > m || (bw == m && br > rm)) {
                     m = bw;
                     rm = br;
@@ -439,6 +516,19 @@ RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 
     return a;
 }
 
+/* 1 / d to within 2^-46 relative (d < 2^40): a float estimate and one Newton
+ * step -- lat_slot's floor correction absorbs any error below one unit */
+RT_HD double lat_rcp(i64 d) {
+#ifdef __CUDA_ARCH__
+    float y0;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y0) : "f"((float)d));
+    const double y = (double)y0;
+    return y * fma(-(double)d, y, 2.0);
+#else
+    return 1.0 / (double)d;
+#endif
+}
+
 /* Least fixed point of r = b + I(r) as the offset N* = r* - b, iterated from
  * N (a lower bound of N*).  -1 = None (suspension.py:123: beyond D),
  * -2 = iteration cap. */
@@ -446,11 +536,13 @@ template <class TM>
 RT_NI double lfp_lat(const TM &tm, const LChains ch, const LBase b, double N, i64 D) {
     RT_COUNT(g_cnt_flfp[ch.res]);
     if (lb_over(b, N, D)) return -1.0;
-    const double invd = b.bf ? 1.0 / (double)b.d : 0.0;
+    const double invd = b.bf ? lat_rcp(b.d) : 0.0;
+    typename TM::Cache cache;
+    tm.cache_reset(cache);
     #pragma unroll 1
     for (int it = 0; it < ITER_CAP; it++) {
         RT_COUNT(g_cnt_fit[ch.res]);
-        const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd);
+        const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd, tm.cache_ptr(cache));
         if (!a.nonint && a.q <= N) return N; /* f(r) <= r with r <= lfp: r is the lfp */
         double Nn = a.q + ceil(a.f + a.rho - 1e-6);
         if (Nn < N + 1.0) Nn = N + 1.0;
@@ -867,6 +959,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         const i64 D = c.D()[k], B = c.B()[k], sClu = c.sClu()[k];
         const Seg32 sg = c.segs(k);
         const Seg32 cl_hi = sg + m, ml_hi = sg + 2 * m + p;
+        const LChains chc = lat_chains(c, k, K_CPU, W), chm = lat_chains(c, k, K_MEM, W);
         int glo = 0, ghi = 0;
         if (gpu) {
             const int gm = c.gmin()[k];
@@ -889,7 +982,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                 bsum += ml_hi[j] + B;
             }
             const LBase lb = {bmax, 0, 1};
-            const double r = lfp_lat(tm, lat_chains(c, k, K_MEM, W), lb, (mw.bi >= 0 && lb_le(mw, lb)) ? mwN : 0.0, D);
+            const double r = lfp_lat(tm, chm, lb, (mw.bi >= 0 && lb_le(mw, lb)) ? mwN : 0.0, D);
             if (r == -2.0) return ST_ESCALATE;
             if (r < 0) {
                 st = RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None at every count */
@@ -916,14 +1009,14 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                     if (p == 0) break;
                     if (sum_mr < 0) {
                         tm.pfor(p, [&](int j) { c.bases()[j] = ml_hi[j] + B; });
-                        sum_mr = lat_chain_sum(tm, c, lat_chains(c, k, K_MEM, W), p, D);
+                        sum_mr = lat_chain_sum(tm, c, chm, p, D);
                         if (sum_mr < 0) return -1; /* -2, or None (impossible: the longest copy's is not) */
                     }
                     if (sum_mr == mr_ub) break;
                     smr = sum_mr;
                 }
                 const LBase b = {gr.bi + smr + sClu, gr.bf, gr.d};
-                const double r = lfp_lat(tm, lat_chains(c, k, K_CPU, W), b, (cw.bi >= 0 && lb_le(cw, b)) ? cwN : 0.0, D);
+                const double r = lfp_lat(tm, chc, b, (cw.bi >= 0 && lb_le(cw, b)) ? cwN : 0.0, D);
                 if (r == -2.0) return -1;
                 if (r >= 0) {
                     cw = b;
@@ -934,7 +1027,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
             /* R1 = GR up + sum MR + sum CR (analysis.py:207); CRs do not depend on g */
             if (sum_cr == -3) {
                 tm.pfor(m, [&](int j) { c.bases()[j] = cl_hi[j]; });
-                sum_cr = lat_chain_sum(tm, c, lat_chains(c, k, K_CPU, W), m, D);
+                sum_cr = lat_chain_sum(tm, c, chc, m, D);
                 if (sum_cr == -2) return -1;
             }
             if (sum_cr < 0) return 0;

@@ -11,8 +11,11 @@ namespace rtgpu {
  * true: the sets the fast kernel handed on in esc[0] (verdict runs), whose
  * decided entries become -1.  Sets the path does not take go on to esc[0]
  * (front) or stay in it (list) for the general stages. */
-template <int W, bool LIST>
-__global__ void __launch_bounds__(256, 4) lattice_kernel(KParams p, int slab_bytes) {
+/* MINB: 256-thread CTAs per SM the register allocation must allow -- 4 (64
+ * registers, 32 warps) for small slabs, 2 (128 registers, no spills in the
+ * fixed-point loop, 16 warps) when shared memory caps residency anyway. */
+template <int W, bool LIST, int MINB>
+__global__ void __launch_bounds__(256, MINB) lattice_kernel(KParams p, int slab_bytes) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int team = warp / W;
@@ -55,29 +58,41 @@ __global__ void __launch_bounds__(256, 4) lattice_kernel(KParams p, int slab_byt
     }
 }
 
-/* team width: the fewest warps per set that keep ~32 warps resident per SM
- * (the register budget at 64 registers) within 227 KB of shared memory */
-static int lat_width(const LSlab &L) {
-    if (L.bytes * 32 <= 220 * 1024) return 1;
-    if (L.bytes * 16 <= 220 * 1024) return 2;
-    return 4;
+/* Kernel shape from the slab size (measured, scripts/gpu_lat_ab.sh r2d:
+ * barriers and spills cost more than occupancy): one warp per set while
+ * 16 slabs fit (32 warps at 64 registers when 32 slabs fit, else 16 warps at
+ * 128), else teams of 2 (or 4) warps at 128 registers. */
+struct LatShape {
+    int W, minb;
+};
+static LatShape lat_shape(const LSlab &L) {
+    const int cap = 220 * 1024;
+    if (L.bytes * 32 <= cap) return {1, 4};
+    if (L.bytes * 16 <= cap) return {1, 2};
+    if (L.bytes * 8 <= cap) return {2, 2};
+    return {4, 2};
 }
 
-template <int W, bool LIST> static void *lat_kernel_ptr() { return (void *)lattice_kernel<W, LIST>; }
+template <int W, bool LIST, int MINB> static void *lat_kernel_ptr() { return (void *)lattice_kernel<W, LIST, MINB>; }
+static void *lat_kernel_for(LatShape sh, bool list) {
+    if (sh.W == 1 && sh.minb == 4) return list ? lat_kernel_ptr<1, true, 4>() : lat_kernel_ptr<1, false, 4>();
+    if (sh.W == 1) return list ? lat_kernel_ptr<1, true, 2>() : lat_kernel_ptr<1, false, 2>();
+    if (sh.W == 2) return list ? lat_kernel_ptr<2, true, 2>() : lat_kernel_ptr<2, false, 2>();
+    return list ? lat_kernel_ptr<4, true, 2>() : lat_kernel_ptr<4, false, 2>();
+}
 
 static int lat_launch(const KParams &p, bool list, cudaStream_t st) {
     LSlab L;
     L.init(p.dims);
-    const int W = lat_width(L);
+    const LatShape sh = lat_shape(L);
+    const int W = sh.W;
     const int teams = 8 / W;
     const int bytes = L.bytes * teams;
     if (bytes > 227 * 1024) {
         set_err_msg("task sets too large for shared memory");
         return -3;
     }
-    void *k = W == 1 ? (list ? lat_kernel_ptr<1, true>() : lat_kernel_ptr<1, false>())
-            : W == 2 ? (list ? lat_kernel_ptr<2, true>() : lat_kernel_ptr<2, false>())
-                     : (list ? lat_kernel_ptr<4, true>() : lat_kernel_ptr<4, false>());
+    void *k = lat_kernel_for(sh, list);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) {
         set_err("cudaFuncSetAttribute", e);

@@ -35,7 +35,7 @@ def compact(blobs, set_off, task_base):
         if b[7] == 0 and all(-2**31 <= v < 2**31 for v in seg):
             recs = b[HDR:base]
             for i in range(n):
-                recs[TW * i + 5] = 2 * base + 2 * (recs[TW * i + 5] - base)
+                recs[TW * i + 5] = 2 * base + (recs[TW * i + 5] - base)  # int32 element offset
             if len(seg) % 2:
                 seg = seg + [0]
             packed = np.asarray(seg, np.int32).view(np.int64).tolist()
