@@ -232,44 +232,36 @@ RT_HD double walk_lat(const double *v, int PM, int half, int p, int h, double H,
     if (H <= 0) return 0;
     const double *P = v, *EP = v + PM + 1;
     const double lim = H + P[h];
-    const double F1 = v[2 * PM + 2];
-    double w0, Hs, nxt;
-    int x;
-    if (F1 > lim) {
-        x = h;
-        Hs = lim;
-        w0 = -EP[h];
-        nxt = F1; /* after the first job's last segment: the second job */
-    } else {
-        const double C = P[p];
-        double r;
-        const double kq = Num<double>::divmod_inv(lim - F1, C, v[2 * PM + 3], r);
-        Hs = r;
-        w0 = EP[p] - EP[h] + kq * EP[p];
-        x = 0;
-        nxt = C; /* the next cycle's first segment */
-    }
-    #pragma unroll 1
-    for (int st = half; st > 0; st >>= 1) {
+    const double F1 = v[2 * PM + 2], C = P[p], EPp = EP[p], EPh = EP[h];
+    /* both cases computed, one selected (no divergence between lanes) */
+    const bool first = F1 > lim;
+    double r;
+    const double kq = Num<double>::divmod_inv(first ? 0.0 : lim - F1, C, v[2 * PM + 3], r);
+    const double Hs = first ? lim : r;
+    const double w0 = first ? -EPh : fma(kq, EPp, EPp - EPh);
+    const double nxt = first ? F1 : C; /* after the last segment: job 2, or the next cycle */
+    int x = first ? h : 0;
+    #pragma unroll
+    for (int st = 16; st > 0; st >>= 1) { /* half <= 16 (PM <= 32) */
         const int y = x + st;
-        if (y <= p - 1 && P[y] <= Hs) x = y;
+        if (st <= half && y <= p - 1 && P[y] <= Hs) x = y;
     }
     const double tail = Hs - P[x];
     const double e0 = EP[x], e1 = EP[x + 1];
-    if (e1 - e0 > tail) {
-        rho = e1 - e0 - tail;
+    const double ex = e1 - e0;
+    if (ex > tail) {
+        rho = ex - tail;
         return w0 + e0 + tail;
     }
     gap = (x < p - 1 ? P[x + 1] : nxt) - Hs;
     return w0 + e1;
 }
 
-
 /* per-iteration accumulators of the interference rounds */
 struct LatAcc {
     double q;    /* sum of floor(W_i) in ticks (exact integers) */
-    double f;    /* sum of the fractional parts in ticks (FP64) */
-    double rho;  /* sum over tasks of a maximising walk's slope-1 length */
+    double f;    /* the fractional parts of the W_i plus every task's slope-1
+                  * length of a maximising walk (ticks, FP64): the jump */
     bool nonint; /* some W_i is not an integer number of ticks */
 };
 
@@ -398,11 +390,7 @@ RT_HD void lat_slot(const LChains &ch, double bN, i64 bf, i64 d, double invd, in
         }
     } else {
         double m1 = NONE, r1 = 0, m0 = 0, vmin = 1e300;
-        #pragma unroll 1
-        for (int h = h0; h < p; h += G) {
-            RT_COUNT(g_cnt_frounds);
-            double r, gp;
-            const double w = walk_lat(v, ch.PM, ch.half, p, h, H, r, gp);
+        auto take = [&](double w, double r, double gp) {
             if (r > 0) {
                 if (w > m1 || (w == m1 && r > r1)) {
                     m1 = w;
@@ -413,6 +401,13 @@ RT_HD void lat_slot(const LChains &ch, double bN, i64 bf, i64 d, double invd, in
                 m0 = tmax(m0, w);
                 vmin = tmin(vmin, gp);
             }
+        };
+        #pragma unroll 1
+        for (int h = h0; h < p; h += G) {
+            RT_COUNT(g_cnt_frounds);
+            double r, gp;
+            const double w = walk_lat(v, ch.PM, ch.half, p, h, H, r, gp);
+            take(w, r, gp);
         }
         if (m1 >= m0) {
             bw = m1;
@@ -436,7 +431,7 @@ RT_HD void lat_slot(const LChains &ch, double bN, i64 bf, i64 d, double invd, in
 template <int W>
 __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &ch, double bN, i64 bf, i64 d,
                                              double invd, LCache &cache) {
-    LatAcc a = {0.0, 0.0, 0.0, false};
+    LatAcc a = {0.0, 0.0, false};
     const int per = 32 >> ch.lg, G = 1 << ch.lg;
     const int R = (ch.k + per - 1) / per;
 #ifdef RTGPU_LAT_NOCACHE
@@ -457,14 +452,13 @@ __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &
             }
         }
         lat_group(bw, s, invs, phv, a); /* every lane of the group holds its task's sums */
-        a.rho += br;
+        a.f += br;
     }
     /* butterfly sums over the groups: identical on every lane (IEEE
      * addition commutes), so the team takes one decision */
     for (int off = G; off < 32; off <<= 1) {
         a.q += shfl_x(a.q, off);
         a.f += shfl_x(a.f, off);
-        a.rho += shfl_x(a.rho, off);
     }
     a.nonint = __any_sync(0xffffffffu, a.nonint);
     if (W > 1) {
@@ -473,17 +467,15 @@ __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &
         if (tm.lane == 0) {
             red[4 * tm.warp + 0] = a.q;
             red[4 * tm.warp + 1] = a.f;
-            red[4 * tm.warp + 2] = a.rho;
             red[4 * tm.warp + 3] = a.nonint ? 1.0 : 0.0;
         }
         tm.sync();
-        a.q = a.f = a.rho = 0;
+        a.q = a.f = 0;
         a.nonint = false;
         #pragma unroll
         for (int w = 0; w < W; w++) { /* the same order in every warp */
             a.q += red[4 * w];
             a.f += red[4 * w + 1];
-            a.rho += red[4 * w + 2];
             a.nonint = a.nonint || red[4 * w + 3] != 0;
         }
     }
@@ -492,7 +484,7 @@ __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &
 #endif
 
 RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 d, double invd, LCache *cache) {
-    LatAcc a = {0.0, 0.0, 0.0, false};
+    LatAcc a = {0.0, 0.0, false};
     const int per = 32 >> ch.lg, G = 1 << ch.lg;
 #ifdef RTGPU_LAT_NOCACHE
     const bool one = false;
@@ -511,7 +503,7 @@ RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 
                 }
             }
             lat_group(m, s, invs, phv, a);
-            a.rho += rm;
+            a.f += rm;
         }
     return a;
 }
@@ -544,7 +536,7 @@ RT_NI double lfp_lat(const TM &tm, const LChains ch, const LBase b, double N, i6
         RT_COUNT(g_cnt_fit[ch.res]);
         const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd, tm.cache_ptr(cache));
         if (!a.nonint && a.q <= N) return N; /* f(r) <= r with r <= lfp: r is the lfp */
-        double Nn = a.q + ceil(a.f + a.rho - 1e-6);
+        double Nn = a.q + ceil(a.f - 1e-6);
         if (Nn < N + 1.0) Nn = N + 1.0;
         if (lb_over(b, Nn, D)) return -1.0;
         N = Nn;

@@ -62,12 +62,19 @@ __global__ void __launch_bounds__(256, MINB) lattice_kernel(KParams p, int slab_
  * barriers and spills cost more than occupancy): one warp per set while
  * 16 slabs fit (32 warps at 64 registers when 32 slabs fit, else 16 warps at
  * 128), else teams of 2 (or 4) warps at 128 registers. */
+#ifndef RTGPU_LAT_SMALL_MINB
+#define RTGPU_LAT_SMALL_MINB 2
+#endif
+#ifndef RTGPU_LAT_MED_MINB
+#define RTGPU_LAT_MED_MINB 2
+#endif
 struct LatShape {
     int W, minb;
 };
 static LatShape lat_shape(const LSlab &L) {
     const int cap = 220 * 1024;
-    if (L.bytes * 32 <= cap) return {1, 4};
+    if (L.bytes * 8 * RTGPU_LAT_SMALL_MINB <= cap) return {1, RTGPU_LAT_SMALL_MINB};
+    if (L.bytes * 8 * RTGPU_LAT_MED_MINB <= cap) return {1, RTGPU_LAT_MED_MINB};
     if (L.bytes * 16 <= cap) return {1, 2};
     if (L.bytes * 8 <= cap) return {2, 2};
     return {4, 2};
@@ -75,7 +82,10 @@ static LatShape lat_shape(const LSlab &L) {
 
 template <int W, bool LIST, int MINB> static void *lat_kernel_ptr() { return (void *)lattice_kernel<W, LIST, MINB>; }
 static void *lat_kernel_for(LatShape sh, bool list) {
-    if (sh.W == 1 && sh.minb == 4) return list ? lat_kernel_ptr<1, true, 4>() : lat_kernel_ptr<1, false, 4>();
+    if (sh.W == 1 && sh.minb == RTGPU_LAT_SMALL_MINB)
+        return list ? lat_kernel_ptr<1, true, RTGPU_LAT_SMALL_MINB>() : lat_kernel_ptr<1, false, RTGPU_LAT_SMALL_MINB>();
+    if (sh.W == 1 && sh.minb == RTGPU_LAT_MED_MINB)
+        return list ? lat_kernel_ptr<1, true, RTGPU_LAT_MED_MINB>() : lat_kernel_ptr<1, false, RTGPU_LAT_MED_MINB>();
     if (sh.W == 1) return list ? lat_kernel_ptr<1, true, 2>() : lat_kernel_ptr<1, false, 2>();
     if (sh.W == 2) return list ? lat_kernel_ptr<2, true, 2>() : lat_kernel_ptr<2, false, 2>();
     return list ? lat_kernel_ptr<4, true, 2>() : lat_kernel_ptr<4, false, 2>();

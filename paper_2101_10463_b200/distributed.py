@@ -62,22 +62,30 @@ def sharded_sweep(cfg: SweepConfig, rank: int = 0, world: int = 1, group=None,
                 if seeds:
                     parts.append(generate_blobs(dataclasses.replace(gen, mem_model=mm), seeds,
                                                 compact=True))
-    local = np.zeros((len(cfg.methods), len(cells)), dtype=np.int64)
+    # one extra column: this rank's count of sets that are neither schedulable
+    # nor unschedulable; it is reduced with the counts, so every rank learns
+    # of a failure after the collective instead of one rank raising before it
+    # and leaving the others blocked in all_reduce
+    local = np.zeros((len(cfg.methods), len(cells) + 1), dtype=np.int64)
     if parts:
         blobs, set_off, task_base = concat_batches(parts)
         for mi, method in enumerate(cfg.methods):
             st = np.asarray(analyze(blobs, set_off, task_base,
                                     METHOD_CODES[AnalysisMethod(method)])).reshape(len(cells), b - a)
-            if np.any((st != SCHEDULABLE) & (st != UNSCHEDULABLE)):
-                raise RuntimeError("undecided task sets in the sweep")
-            local[mi] = (st == SCHEDULABLE).sum(axis=1)
+            local[mi, :-1] = (st == SCHEDULABLE).sum(axis=1)
+            local[mi, -1] = int(np.sum((st != SCHEDULABLE) & (st != UNSCHEDULABLE)))
     counts = torch.from_numpy(local)
+    if world > 1:
+        import torch.distributed as dist
+        if device is None and dist.get_backend(group) == "nccl":
+            device = torch.device("cuda", torch.cuda.current_device())  # NCCL reduces device tensors only
     if device is not None:
         counts = counts.to(device)
     if world > 1:
-        import torch.distributed as dist
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     counts = counts.cpu().numpy()
+    if counts[:, -1].any():
+        raise RuntimeError(f"{int(counts[:, -1].sum())} undecided task sets in the sweep")
     rows = []
     ci = 0
     per = cfg.tasksets_per_point
