@@ -25,7 +25,7 @@
  *   analysis.analyze_self_suspension_baseline  analysis.py:319  (RTGPU_METHOD_SELFSUSP)
  *   analysis.analyze_busy_waiting_baseline     analysis.py:355  (RTGPU_METHOD_BUSYWAIT)
  *   suspension.{workload,max_workload,         suspension.py:107-176
- *               segment_response,task_response}   rtgpu_susp_{host,device}
+ *               segment_response,task_response}   rtgpu_query_host (RTGPU_Q_*)
  *
  * ---------------------------------------------------------------------
  * Packed task-set layout ("blob"), shared by the engine and the oracle.
@@ -123,7 +123,10 @@ int rtgpu_device_info(int *n_devices, int *sm_count, int *cc_major, int *cc_mino
  * from a sample of the batch and sets beyond it are re-run at the batch's
  * true sizes.  Other runs pipeline per-chunk launches over two streams.
  * e2e_num / den are written only with RTGPU_F_BOUNDS or RTGPU_F_DETAIL.
- * eval_budget <= 0 means unlimited.  Returns 0 or a negative error code.
+ * eval_budget <= 0 means unlimited (the search always ends: the allocation
+ * space is finite); > 0 caps the task evaluations of an irregular set's
+ * depth-first search (RTGPU_UNDECIDED beyond).  Returns 0 or a negative
+ * error code.
  */
 int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off,
                        const int64_t *task_base, int64_t n_sets, int method,

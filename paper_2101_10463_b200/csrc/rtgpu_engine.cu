@@ -185,7 +185,7 @@ int run_device(const i64 *d_blobs, const i64 *d_set_off, const i64 *d_task_base,
     p.GM = pow2_group(dims.MP > 0 ? dims.MP : 1);
     p.flags = flags;
     p.method = method;
-    p.budget = budget > 0 ? budget : (i64)1 << 22;
+    p.budget = budget > 0 ? budget : 0; /* <= 0: unlimited, as the reference (it enumerates every allocation) */
     p.status = d_status;
     p.evals = d_evals;
     p.vsm = d_vsm;
@@ -402,7 +402,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
     p.GM = pow2_group(d.MP > 0 ? d.MP : 1);
     p.flags = flags;
     p.method = method;
-    p.budget = eval_budget > 0 ? eval_budget : (i64)1 << 22;
+    p.budget = eval_budget > 0 ? eval_budget : 0; /* <= 0: unlimited */
     p.status = (int32_t *)g_h_status.p;
     p.evals = (i64 *)g_h_evals.p;
     p.vsm = (int32_t *)g_h_vsm.p;

@@ -71,11 +71,11 @@ def compare(o, e, so, tb, bounds):
 def shapes(rng):
     """(label, generator) pairs, small platforms first (full enumeration)."""
     out = []
-    for gn in (4, 6, 8, 10, 12):
-        for n in (3, 4, 5, 6):
+    for gn in (4, 6, 8, 10):
+        for n in (3, 4, 5):
             out.append(("full", n, gn))
     for gn in (16, 24, 32, 48):
-        for n in (6, 8, 10):
+        for n in (6, 8):
             out.append(("prefix", n, gn))
     rng.shuffle(out)
     return out
@@ -86,7 +86,7 @@ def main():
     ap.add_argument("--minutes", type=float, default=20.0)
     ap.add_argument("--log", default=os.path.join(ROOT, "gpurun_out", "parity_scale.jsonl"))
     ap.add_argument("--seed", type=int, default=11)
-    ap.add_argument("--budget", type=int, default=100000)
+    ap.add_argument("--budget", type=int, default=50000)
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.log), exist_ok=True)
     oracle.build()
@@ -104,7 +104,7 @@ def main():
                 mm = int(rng.integers(0, 2))
                 m = int(rng.integers(2, 7))
                 kind = ["gen", "adv", "adv-irreg"][rnd % 3]
-                count = 4000 if mode == "full" else 400
+                count = 5000 if mode == "full" else 500
                 seed = args.seed * 100003 + rnd
                 if kind == "gen":
                     u = Fraction(int(rng.integers(1, 11)), 10)

@@ -56,7 +56,7 @@ int run_one(const Dims &d, const i64 *blob, int method, unsigned flags, i64 budg
     c.MC = d.MC;
     c.MP = d.MP;
     set_groups(c);
-    c.budget = budget > 0 ? budget : (i64)1 << 22;
+    c.budget = budget > 0 ? budget : 0;
     c.method = method;
     SeqTeam tm;
     int st = analyze_set(tm, c, flags, o);
@@ -104,7 +104,7 @@ extern "C" int host_analyze_batch(const int64_t *blobs, const int64_t *set_off,
             c.MC = d.MC;
             c.MP = d.MP;
             set_groups(c);
-            c.budget = budget > 0 ? budget : (i64)1 << 22;
+            c.budget = budget > 0 ? budget : 0;
             c.method = method;
             SeqTeam tm;
             st = fast_verdict(tm, c, vsm + tb);
