@@ -62,9 +62,34 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     return lib
 
 
+TORCH_OP = os.path.join(HERE, "rtgpu_torch.so")
+
+
+def build_torch_op(force: bool = False, verbose: bool = False) -> str:
+    """The PyTorch operator torch.ops.rtgpu.analyze_out (csrc/torch_ops.cpp),
+    an in-tree shared library linked against librtgpu.so."""
+    src = os.path.join(CSRC, "torch_ops.cpp")
+    if not force and os.path.exists(TORCH_OP) and all(
+            os.path.getmtime(p) <= os.path.getmtime(TORCH_OP)
+            for p in (src, LIB, os.path.join(ROOT, "include", "rtgpu.h"))):
+        return TORCH_OP
+    from torch.utils import cpp_extension
+    bdir = os.path.join(HERE, "build", "torch_op")
+    os.makedirs(bdir, exist_ok=True)
+    cpp_extension.load(name="rtgpu_torch", sources=[src], build_directory=bdir,
+                       extra_include_paths=[os.path.join(ROOT, "include")],
+                       extra_cflags=["-O2"], extra_ldflags=[f"-L{HERE}", "-lrtgpu", "-Wl,-rpath,$ORIGIN", f"-Wl,-rpath,{HERE}"],
+                       with_cuda=True, is_python_module=False, verbose=verbose)
+    built = os.path.join(bdir, "rtgpu_torch.so")
+    os.replace(built, TORCH_OP)
+    return TORCH_OP
+
+
 if __name__ == "__main__":
     # python -m paper_2101_10463_b200.build [--force] [--out PATH -DNAME=VAL ...]
     argv = sys.argv[1:]
     out = argv[argv.index("--out") + 1] if "--out" in argv else None
     defs = [a[2:] for a in argv if a.startswith("-D")]
     print(build(force="--force" in argv or out is not None, verbose=True, out=out, defines=defs))
+    if out is None and "--no-torch-op" not in argv:
+        print(build_torch_op(force="--force" in argv))

@@ -8,6 +8,7 @@ through ``rtgpu_analyze_host``.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -17,6 +18,26 @@ from . import _native
 from .pack import F_BOUNDS, F_DETAIL, RawResults
 
 METHOD_RTGPU, METHOD_SELFSUSP, METHOD_BUSYWAIT = 0, 1, 2
+
+_OP_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "rtgpu_torch.so")
+_op = None
+
+
+def torch_op():
+    """torch.ops.rtgpu.analyze_out (csrc/torch_ops.cpp: rtgpu_analyze_device as
+    a PyTorch operator on the current stream), or None when an A/B build is
+    selected with RTGPU_LIB (the operator links the in-tree library) or the
+    operator is not built."""
+    global _op
+    if _op is None:
+        if os.environ.get("RTGPU_LIB") or not os.path.exists(_OP_PATH):
+            _op = False
+        else:
+            import torch
+            _native.lib()  # the same librtgpu.so instance the operator links
+            torch.ops.load_library(_OP_PATH)
+            _op = torch.ops.rtgpu.analyze_out
+    return _op or None
 
 
 def batch_dims(blobs: np.ndarray, set_off: np.ndarray) -> tuple[int, int, int]:
@@ -74,6 +95,12 @@ class DeviceBatch:
             torch.empty(self.n_tasks, dtype=torch.int64, device=d),
             torch.empty(self.words, dtype=torch.int64, device=d) if detail else None)
 
+    def _no_detail(self):
+        import torch
+        if getattr(self, "_empty", None) is None:
+            self._empty = torch.empty(0, dtype=torch.int64, device=self.device)
+        return self._empty
+
     def output_bytes(self, flags: int) -> int:
         b = 4 * self.n_sets + 8 * self.n_sets + 4 * self.n_tasks
         if flags & (F_BOUNDS | F_DETAIL):
@@ -88,6 +115,13 @@ class DeviceBatch:
         import torch
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
+        op = torch_op()
+        if op is not None:
+            with torch.cuda.stream(stream):
+                op(self.blobs, self.set_off, self.task_base, self.dims[0], self.dims[1], self.dims[2],
+                   method, flags, budget, out.status, out.evals, out.vsm, out.e2e_num, out.den,
+                   out.detail if out.detail is not None else self._no_detail())
+            return
         _native.analyze_device(
             self.blobs.data_ptr(), self.set_off.data_ptr(), self.task_base.data_ptr(),
             self.n_sets, self.dims, method, flags, budget, out.status.data_ptr(),

@@ -44,3 +44,14 @@ def test_no_cpu_fallback():
     from paper_2101_10463_b200.model import PlatformConfig, TaskSet, MemModel
     with pytest.raises(_native.EngineUnavailable):
         analyze_rtgpu(TaskSet((), MemModel.TWO_COPY, PlatformConfig(4)))
+
+
+def test_torch_operator_registers():
+    """The PyTorch operator (csrc/torch_ops.cpp) loads and registers
+    rtgpu::analyze_out with its schema (no compute without a GPU)."""
+    import torch
+    from paper_2101_10463_b200 import build
+    torch.ops.load_library(build.build_torch_op())
+    op = torch.ops.rtgpu.analyze_out
+    schema = str(op.default._schema)
+    assert "Tensor(a!) status" in schema and "int budget" in schema
