@@ -62,6 +62,21 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     return lib
 
 
+def build_packer(force: bool = False) -> str:
+    """The CPython extension paper_2101_10463_b200._packer (csrc/packer.cpp):
+    TaskSet objects -> blobs without Python-level field walking."""
+    import sysconfig
+    out = os.path.join(HERE, "_packer" + sysconfig.get_config_var("EXT_SUFFIX"))
+    src = os.path.join(CSRC, "packer.cpp")
+    if not force and os.path.exists(out) and os.path.getmtime(src) <= os.path.getmtime(out):
+        return out
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared",
+           "-I", sysconfig.get_paths()["include"], src, "-o", out + ".tmp"]
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 TORCH_OP = os.path.join(HERE, "rtgpu_torch.so")
 
 
@@ -93,3 +108,5 @@ if __name__ == "__main__":
     print(build(force="--force" in argv or out is not None, verbose=True, out=out, defines=defs))
     if out is None and "--no-torch-op" not in argv:
         print(build_torch_op(force="--force" in argv))
+    if out is None:
+        print(build_packer(force="--force" in argv))

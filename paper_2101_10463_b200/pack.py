@@ -192,6 +192,31 @@ def pack_set(ts: TaskSet) -> tuple[list[int], int, tuple]:
 
 
 def pack_tasksets(tasksets: Sequence[TaskSet]) -> PackedBatch:
+    """The batch of blobs: the native packer (csrc/packer.cpp, the same
+    words) when built; a set it refuses (values beyond int64, a shape the
+    engine does not take) is packed by pack_set for the exact exception."""
+    try:
+        from . import _packer
+    except ImportError:
+        _packer = None
+    if _packer is not None and tasksets:
+        try:
+            b, so, tb, scales, orders = _packer.pack(tasksets)
+        except (ValueError, OverflowError, TypeError, AttributeError):
+            pass
+        else:
+            blobs = np.frombuffer(b, dtype=np.int64)
+            set_off = np.frombuffer(so, dtype=np.int64)
+            task_base = np.frombuffer(tb, dtype=np.int64)
+            metas = [SetMeta(ts, tuple(ts.tasks[i] for i in order), int(S), int(set_off[k]),
+                             int(task_base[k]))
+                     for k, (ts, S, order) in enumerate(zip(tasksets, scales, orders))]
+            return PackedBatch(blobs, set_off, task_base, metas)
+    return pack_tasksets_py(tasksets)
+
+
+def pack_tasksets_py(tasksets: Sequence[TaskSet]) -> PackedBatch:
+    """Python packer (reference for the native one; exact exceptions)."""
     words: list[int] = []
     set_off = [0]
     task_base = [0]
