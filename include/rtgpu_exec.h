@@ -97,6 +97,13 @@ int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items,
                                 int idle_us, const uint32_t *bg_mask, float *ms_out,
                                 int32_t *blocks_out, int32_t *sms_out);
 
+/* Same, with a host thread alternating H2D / D2H pinned copies of
+ * copy_bytes on its own stream throughout (copy-engine, L2 and memory
+ * load of the other tasks' copies); copy_bytes <= 0: no copies. */
+int rtgpu_exec_kernel_ms_stress(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
+                                int idle_us, const uint32_t *bg_mask, int64_t copy_bytes, float *ms_out,
+                                int32_t *blocks_out, int32_t *sms_out);
+
 /* Host wall time (us) of `reps` empty segment launches on `mask`: memset,
  * launch and polled completion -- the executor's per-kernel overhead. */
 int rtgpu_exec_launch_us(const uint32_t *mask, int reps, float *us_out);

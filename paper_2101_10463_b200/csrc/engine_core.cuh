@@ -629,7 +629,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
  * wait.  Integer-valued doubles below 2^52: the sums are exact in any
  * order, so the view is identical to build_view's. */
 template <class V>
-__device__ __noinline__ void build_view_warp(SetCtx<V> &c, int i, i64 q, int lane) {
+__device__ __forceinline__ void build_view_warp_body(SetCtx<V> &c, int i, i64 q, int lane) {
     typedef Num<V> N;
     const TaskRec &t = c.TR()[i];
     const Seg32 sg{(const int32_t *)c.blob + t.seg};
@@ -715,6 +715,29 @@ __device__ __noinline__ void build_view_warp(SetCtx<V> &c, int i, i64 q, int lan
         }
     }
     __syncwarp();
+}
+
+/* The out-of-line entry of build_view_warp_body: the set context is rebuilt
+ * from scalars, so the caller's SetCtx never has its address taken and stays
+ * in registers (a SetCtx passed by reference to an out-of-line routine lives
+ * in the stack frame, whose dirty lines were the fast kernel's DRAM write
+ * traffic). */
+template <class V>
+__device__ __noinline__ void build_view_warp_s(const i64 *blob, int o_tr, int o_vc, int o_vm, int SC, int SM,
+                                              int MC, int MP, int mm, int i, i64 q, int lane) {
+    SetCtx<V> c;
+    c.blob = blob;
+    c.hbase = nullptr;
+    c.o_tr = o_tr;
+    c.o_vc = o_vc;
+    c.o_vm = o_vm;
+    c.L.SC = SC;
+    c.L.SM = SM;
+    c.MC = MC;
+    c.MP = MP;
+    c.mm = mm;
+    c.segw = 1;
+    build_view_warp_body(c, i, q, lane);
 }
 #endif
 
@@ -866,7 +889,9 @@ RT_HD V interference(const TM &tm, const IView<V> &iv, V H, V &rho, bool &err) {
 template <class V, class TM>
 RT_NI V lfp(const TM &tm, SetCtx<V> &c, int k, int kind, V base, V start, V bound) {
     RT_COUNT(g_cnt_lfp[kind]);
-    if (base > bound) return (V)-1;
+    /* a warm start is a lower bound of the lfp: beyond the bound, the
+     * reference's iteration from `base` would pass it too (None) */
+    if (base > bound || start > bound) return (V)-1;
     const IView<V> iv = make_iview(c, k, kind);
     V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
@@ -1715,7 +1740,7 @@ RT_NI int search_baseline(const TM &tm, SetCtx<V> &c) {
  * ranges (segments >= 2^31, A >= 2^16, D or T >= 2^56) mark the task
  * TF_UNSUP, which sends the set to the general path (128-bit load). */
 template <class V>
-RT_NI void load_task_fast(SetCtx<V> &c, int i) {
+RT_HD void load_task_fast_body(SetCtx<V> &c, int i) {
     const i64 *r = c.blob + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
     TaskRec &t = c.TR()[i];
     t.m = (int)r[0];
@@ -1817,11 +1842,27 @@ RT_NI void load_task_fast(SetCtx<V> &c, int i) {
     }
 }
 
+/* out-of-line entry with scalar arguments (see build_view_warp_s) */
+template <class V>
+RT_NI void load_task_fast_s(const i64 *blob, unsigned char *hbase, int o_tr, int mm, int MC, int MP, i64 A,
+                            int GN, int i) {
+    SetCtx<V> c;
+    c.blob = blob;
+    c.hbase = hbase;
+    c.o_tr = o_tr;
+    c.mm = mm;
+    c.MC = MC;
+    c.MP = MP;
+    c.A = A;
+    c.GN = GN;
+    load_task_fast_body(c, i);
+}
+
 /* least fixed point on a fixed scale; -1 = None, -2 = iteration cap */
 template <class V, class TM>
 RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kind, int lg,
                  int PM, int half, int stride, V base, V start, V bound) {
-    if (base > bound) return (V)-1;
+    if (base > bound || start > bound) return (V)-1; /* start: a lower bound of the lfp */
     RT_COUNT(g_cnt_flfp[kind]);
     V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
@@ -1879,7 +1920,12 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         return ST_ESCALATE; /* GN > 64: the fixed scale almost never fits (gtop > 42); skip the
                              * task loads and take the general path's per-task scales */
     TaskRec *tr = c.TR();
-    tm.pfor(n, [&](int i) { load_task_fast(c, i); });
+    {
+        const i64 *blob = c.blob;
+        unsigned char *hb = c.hbase;
+        const int o_tr = c.o_tr, mm = c.mm, MC = c.MC, MP = c.MP;
+        tm.pfor(n, [&](int i) { load_task_fast_s<V>(blob, hb, o_tr, mm, MC, MP, A, GN, i); });
+    }
     i64 vb_max = 0, need = 0;
     #pragma unroll 1
     for (int k = 0; k < n; k++)
@@ -1942,7 +1988,9 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         const TaskRec &t = tr[k];
         /* views of tasks before k (their counts are final) */
 #ifdef __CUDA_ARCH__
-        if (k > 0) build_view_warp(c, k - 1, q, tm.lane);
+        if (k > 0)
+            build_view_warp_s<V>(c.blob, c.o_tr, c.o_vc, c.o_vm, c.L.SC, c.L.SM, c.MC, c.MP, c.mm, k - 1, q,
+                                 tm.lane);
 #else
         if (k > 0) tm.pfor(1, [&](int) { build_view<V, Seg32>(c, k - 1, q); });
 #endif

@@ -468,6 +468,45 @@ int rtgpu_exec_kernel_ms_idle(const uint32_t *mask, int nslots, int64_t items, i
 int rtgpu_exec_kernel_ms_loaded(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
                                 int idle_us, const uint32_t *bg_mask, float *ms_out,
                                 int32_t *blocks_out, int32_t *sms_out) {
+    return rtgpu_exec_kernel_ms_stress(mask, nslots, items, iters, reps, idle_us, bg_mask, 0, ms_out,
+                                       blocks_out, sms_out);
+}
+
+int rtgpu_exec_kernel_ms_stress(const uint32_t *mask, int nslots, int64_t items, int iters, int reps,
+                                int idle_us, const uint32_t *bg_mask, int64_t copy_bytes, float *ms_out,
+                                int32_t *blocks_out, int32_t *sms_out) {
+    /* copy load: a host thread keeps alternating H2D / D2H copies of
+     * copy_bytes (pinned) on its own stream for the whole measurement -- the
+     * executor's other tasks move their data while a kernel runs, loading
+     * the copy engines, L2 and the memory controllers */
+    std::atomic<bool> stop_copies{false};
+    std::thread copier;
+    Lane C;
+    if (copy_bytes > 0) {
+        if (lane_init(C, (size_t)copy_bytes)) {
+            strcpy(g_err, "executor allocation failed");
+            return -1;
+        }
+        copier = std::thread([&]() {
+            for (int k = 0; !stop_copies.load(std::memory_order_relaxed); k++) {
+                if (k & 1) cudaMemcpyAsync(C.hbuf, C.dbuf, (size_t)copy_bytes, cudaMemcpyDeviceToHost, C.st);
+                else cudaMemcpyAsync(C.dbuf, C.hbuf, (size_t)copy_bytes, cudaMemcpyHostToDevice, C.st);
+                cudaStreamSynchronize(C.st);
+            }
+        });
+    }
+    struct Joiner {
+        std::atomic<bool> &stop;
+        std::thread &t;
+        Lane &c;
+        bool on;
+        ~Joiner() {
+            if (!on) return;
+            stop.store(true);
+            t.join();
+            lane_free(c);
+        }
+    } joiner{stop_copies, copier, C, copy_bytes > 0};
     Lane L;
     if (lane_init(L, 64)) {
         strcpy(g_err, "executor allocation failed");

@@ -14,8 +14,12 @@ namespace rtgpu {
 /* MINB: 256-thread CTAs per SM the register allocation must allow -- 4 (64
  * registers, 32 warps) for small slabs, 2 (128 registers, no spills in the
  * fixed-point loop, 16 warps) when shared memory caps residency anyway. */
+#ifndef RTGPU_LAT_THREADS
+#define RTGPU_LAT_THREADS 256 /* CTA size: RTGPU_LAT_THREADS / 32 / W teams per CTA */
+#endif
+
 template <int W, bool LIST, int MINB>
-__global__ void __launch_bounds__(256, MINB) lattice_kernel(KParams p, int slab_bytes) {
+__global__ void __launch_bounds__(RTGPU_LAT_THREADS, MINB) lattice_kernel(KParams p, int slab_bytes) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int team = warp / W;
@@ -72,12 +76,12 @@ struct LatShape {
     int W, minb;
 };
 static LatShape lat_shape(const LSlab &L) {
-    const int cap = 220 * 1024;
-    if (L.bytes * 8 * RTGPU_LAT_SMALL_MINB <= cap) return {1, RTGPU_LAT_SMALL_MINB};
-    if (L.bytes * 8 * RTGPU_LAT_MED_MINB <= cap) return {1, RTGPU_LAT_MED_MINB};
-    if (L.bytes * 16 <= cap) return {1, 2};
-    if (L.bytes * 8 <= cap) return {2, 2};
-    return {4, 2};
+    const int cap = 220 * 1024, wpc = RTGPU_LAT_THREADS / 32; /* warps per CTA */
+    if (L.bytes * wpc * RTGPU_LAT_SMALL_MINB <= cap) return {1, RTGPU_LAT_SMALL_MINB};
+    if (L.bytes * wpc * RTGPU_LAT_MED_MINB <= cap) return {1, RTGPU_LAT_MED_MINB};
+    if (L.bytes * 16 <= cap) return {1, RTGPU_LAT_MED_MINB};
+    if (L.bytes * 8 <= cap) return {2, RTGPU_LAT_MED_MINB};
+    return {4, RTGPU_LAT_MED_MINB};
 }
 
 template <int W, bool LIST, int MINB> static void *lat_kernel_ptr() { return (void *)lattice_kernel<W, LIST, MINB>; }
@@ -86,9 +90,9 @@ static void *lat_kernel_for(LatShape sh, bool list) {
         return list ? lat_kernel_ptr<1, true, RTGPU_LAT_SMALL_MINB>() : lat_kernel_ptr<1, false, RTGPU_LAT_SMALL_MINB>();
     if (sh.W == 1 && sh.minb == RTGPU_LAT_MED_MINB)
         return list ? lat_kernel_ptr<1, true, RTGPU_LAT_MED_MINB>() : lat_kernel_ptr<1, false, RTGPU_LAT_MED_MINB>();
-    if (sh.W == 1) return list ? lat_kernel_ptr<1, true, 2>() : lat_kernel_ptr<1, false, 2>();
-    if (sh.W == 2) return list ? lat_kernel_ptr<2, true, 2>() : lat_kernel_ptr<2, false, 2>();
-    return list ? lat_kernel_ptr<4, true, 2>() : lat_kernel_ptr<4, false, 2>();
+    if (sh.W == 2)
+        return list ? lat_kernel_ptr<2, true, RTGPU_LAT_MED_MINB>() : lat_kernel_ptr<2, false, RTGPU_LAT_MED_MINB>();
+    return list ? lat_kernel_ptr<4, true, RTGPU_LAT_MED_MINB>() : lat_kernel_ptr<4, false, RTGPU_LAT_MED_MINB>();
 }
 
 static int lat_launch(const KParams &p, bool list, cudaStream_t st) {
@@ -96,7 +100,7 @@ static int lat_launch(const KParams &p, bool list, cudaStream_t st) {
     L.init(p.dims);
     const LatShape sh = lat_shape(L);
     const int W = sh.W;
-    const int teams = 8 / W;
+    const int teams = RTGPU_LAT_THREADS / 32 / W;
     const int bytes = L.bytes * teams;
     if (bytes > 227 * 1024) {
         set_err_msg("task sets too large for shared memory");
@@ -111,7 +115,7 @@ static int lat_launch(const KParams &p, bool list, cudaStream_t st) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, RTGPU_LAT_THREADS, bytes);
     if (per_sm < 1) per_sm = 1;
     i64 grid = (i64)sms * per_sm;
     if (!list) {
@@ -121,7 +125,7 @@ static int lat_launch(const KParams &p, bool list, cudaStream_t st) {
     if (grid < 1) grid = 1;
     int sb = L.bytes;
     void *args[] = {(void *)&p, (void *)&sb};
-    e = cudaLaunchKernel(k, dim3((unsigned)grid), dim3(256), args, bytes, st);
+    e = cudaLaunchKernel(k, dim3((unsigned)grid), dim3(RTGPU_LAT_THREADS), args, bytes, st);
     count_launch();
     if (e != cudaSuccess) {
         set_err("lattice_kernel launch", e);

@@ -76,6 +76,12 @@ def _lib():
                                                   ctypes.POINTER(ctypes.c_float),
                                                   ctypes.POINTER(ctypes.c_int32),
                                                   ctypes.POINTER(ctypes.c_int32)]
+        L.rtgpu_exec_kernel_ms_stress.argtypes = [ctypes.POINTER(ctypes.c_uint32), ctypes.c_int,
+                                                  ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_int, ctypes.POINTER(ctypes.c_uint32),
+                                                  ctypes.c_int64, ctypes.POINTER(ctypes.c_float),
+                                                  ctypes.POINTER(ctypes.c_int32),
+                                                  ctypes.POINTER(ctypes.c_int32)]
         L.rtgpu_exec_copy_ms.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_float)]
         L.rtgpu_exec_run.argtypes = [ctypes.POINTER(ExecTaskC), ctypes.c_int, ctypes.c_double,
@@ -103,6 +109,20 @@ def kernel_ms_loaded(sms, bg_sms, nslots: int, items: int, iters: int, reps: int
     rc = _lib().rtgpu_exec_kernel_ms_loaded(mask_of(sms), nslots, items, iters, reps, 0,
                                             mask_of(bg_sms), out, ctypes.byref(nb),
                                             ctypes.byref(ns))
+    if rc:
+        raise RuntimeError(_lib().rtgpu_exec_last_error().decode())
+    return [float(x) for x in out], nb.value, ns.value
+
+
+def kernel_ms_stress(sms, bg_sms, copy_bytes: int, nslots: int, items: int, iters: int, reps: int = 3):
+    """Like kernel_ms_loaded with, in addition, H2D / D2H copies of copy_bytes
+    running back to back on another stream (the other tasks' copies)."""
+    _native.require_device()
+    out = (ctypes.c_float * reps)()
+    nb, ns = ctypes.c_int32(0), ctypes.c_int32(0)
+    rc = _lib().rtgpu_exec_kernel_ms_stress(mask_of(sms), nslots, items, iters, reps, 0,
+                                            mask_of(bg_sms) if bg_sms else None, copy_bytes, out,
+                                            ctypes.byref(nb), ctypes.byref(ns))
     if rc:
         raise RuntimeError(_lib().rtgpu_exec_last_error().decode())
     return [float(x) for x in out], nb.value, ns.value
@@ -168,6 +188,7 @@ class WcrtReport:
     kernels_within_bound: bool = False
     max_ratio: float = 0.0
     max_kernel_ratio: float = 0.0  # worst measured kernel time / its Lemma-4 bound
+    sms_used: int = 0              # physical SMs covered by the partitions
     horizon_us: float = 0.0
     cpu_mode: int = CPU_PARALLEL
     bus_mode: int = BUS_FP
@@ -191,9 +212,12 @@ MARGIN = 0.25
 
 
 def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = MARGIN,
-                     idle_us: int = 20000) -> KernelCal:
+                     idle_us: int = 20000, copy_bytes: int = 4 << 20) -> KernelCal:
     """Worst case over SMs of both dies, warm launches and launches after an
-    idle GPU (the SM clock may have dropped; clocks are not locked here)."""
+    idle GPU (the SM clock may have dropped; clocks are not locked here), with
+    co-runners on every other SM, and with co-runners plus back-to-back
+    H2D / D2H copies (the conditions of a run: other partitions compute while
+    other tasks copy)."""
     t1, t2 = [], []
     for sm in CAL_SMS:
         others = [x for x in range(148) if x != sm]
@@ -202,6 +226,9 @@ def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = MARG
         # co-runners on every other SM (the executor's concurrent partitions)
         t1 += kernel_ms_loaded([sm], others, 1, items, iters, 2)[0]
         t2 += kernel_ms_loaded([sm], others, 2, items, iters, 2)[0]
+        if copy_bytes > 0:
+            t1 += kernel_ms_stress([sm], others, copy_bytes, 1, items, iters, 2)[0]
+            t2 += kernel_ms_stress([sm], others, copy_bytes, 2, items, iters, 2)[0]
     t1u, t2u = max(t1) * 1e3, max(t2) * 1e3
     pct = math.ceil(200 * t2u / t1u)
     if pct > 180:  # MAX_INTERLEAVE_RATIO (model.py:17): the model cannot bound this kernel
@@ -250,22 +277,30 @@ def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = 
 def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int = 0,
                     utilization: float = 3.0, horizon_us: float = 3e6, n_sm: int = 148,
                     margin: float = MARGIN, cpu_mode: int = CPU_PARALLEL,
-                    bus_mode: int = BUS_FP, layout: str = "") -> WcrtReport:
+                    bus_mode: int = BUS_FP, layout: str = "", width=None) -> WcrtReport:
     """BASELINE config 4: n concurrent tasks on disjoint SM partitions of the
     GPU; measured WCRT vs the RTGPU bound R_k.  layout "consecutive" packs
     the partitions on consecutive SM ids; "tpc" gives each task whole TPCs
     (SM pairs 2t, 2t+1), so no two tasks share a TPC (default: $RTGPU_EXEC_LAYOUT,
     else "tpc").  Over 72 robustness runs each layout saw occasional kernel
     overruns of Lemma 4 (tpc 4, consecutive 4 in 48); only consecutive
-    partitions pushed a job past R_k (2 runs) -- profiles/r1m_exec_*.jsonl."""
+    partitions pushed a job past R_k (2 runs) -- profiles/r1m_exec_*.jsonl.
+
+    width = (lo, hi): wide partitions -- kernels sized so that one SM would
+    need tens of milliseconds, and every task's deadline set from a target
+    SM count drawn from [lo, hi] (its own segments at that count, times a
+    slack for the interference of higher-priority tasks), so the analysis
+    gives each task a partition of several to tens of SMs; `utilization`
+    is then unused."""
     _native.require_device()
     rng = np.random.default_rng(seed)
     defs = []
+    items_rng = (400, 3000) if width is None else (6000, 20000)
     for i in range(n_tasks):
         defs.append(ExecTaskDef(
             cpu_us=[int(x) for x in rng.integers(100, 600, m)],
             copy_bytes=[int(x) for x in rng.integers(1 << 18, 4 << 20, 2 * m - 2)],
-            kernel_items=[int(x) for x in rng.integers(400, 3000, m - 1)]))
+            kernel_items=[int(x) for x in rng.integers(*items_rng, m - 1)]))
     # calibrate every kernel and copy on the device
     cal = {}
     for d in defs:
@@ -277,6 +312,12 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
     overhead = max(launch_us(list(range(8)), 50) +
                    [x * 1e3 for x in kernel_ms(list(range(8)), 2, 0, iters, 3, 20000)[0]])
     GL = _ceil_margin(overhead, margin)
+    # a kernel's blocks claim work items one at a time, so the last item
+    # can end up to one item's two-slot time tau2 = 2 t2 / items after the
+    # perfectly divided (C - L)/m of Lemma 4: the critical-path term of a
+    # kernel carries it (L (1 - 1/2g) >= launch + tau2 for L = 2 (launch +
+    # tau2)); it matters once partitions are wide and items per block few
+    gl_of = {it: _ceil_margin(2 * (overhead + 2 * c.t2_us / c.items), margin) for it, c in cal.items()}
     copy_cal = {}
     for d in defs:
         for j, b in enumerate(d.copy_bytes):
@@ -288,6 +329,11 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
     specs = []
     util = rng.uniform(0.5, 1.5, n_tasks)
     util = util / util.sum() * utilization
+    targets = None
+    if width is not None:
+        targets = rng.integers(width[0], width[1] + 1, n_tasks)
+        while targets.sum() > n_sm - 2 * n_tasks:  # room for TPC alignment
+            targets = np.maximum(1, targets - 1)
     for i, d in enumerate(defs):
         cpu = tuple(ExecBounds.exact(c) for c in d.cpu_us)
         mem = tuple(ExecBounds(Fraction(copy_cal[(b, j % 2 == 0)][0]),
@@ -295,10 +341,15 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
                     for j, b in enumerate(d.copy_bytes))
         gpu = tuple(GpuKernelModel(ExecBounds(Fraction(min(cal[it].lo_us, cal[it].hi_us)),
                                               Fraction(cal[it].hi_us)),
-                                   Fraction(min(GL, cal[it].lo_us)), cal[it].alpha)
+                                   Fraction(min(gl_of[it], cal[it].lo_us)), cal[it].alpha)
                     for it in d.kernel_items)
         demand = sum(c.hi for c in cpu) + sum(x.hi for x in mem) + sum(g.work.hi for g in gpu)
-        D = int(demand / Fraction(util[i]).limit_denominator(10**6))
+        if targets is None:
+            D = int(demand / Fraction(util[i]).limit_denominator(10**6))
+        else:
+            own = (sum(c.hi for c in cpu) + sum(x.hi for x in mem) +
+                   sum(gpu_response_bounds(g, 2 * int(targets[i])).hi for g in gpu))
+            D = int(own * Fraction(rng.uniform(1.5, 2.2)).limit_denominator(1000)) + 1
         d.period_us = d.deadline_us = D
         specs.append(TaskSpec(f"x{i}", cpu, mem, gpu, Fraction(D), Fraction(D), 0))
     order = sorted(range(n_tasks), key=lambda i: (specs[i].deadline, i))
@@ -308,8 +359,10 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
     report = analyze_rtgpu(ts)
     out = WcrtReport(schedulable=report.schedulable, horizon_us=horizon_us)
     out.calibration = [{"items": c.items, "t1_us": round(c.t1_us, 1), "t2_us": round(c.t2_us, 1),
-                        "alpha": str(c.alpha), "gw_hi_us": c.hi_us, "gl_us": GL}
-                       for c in cal.values()]
+                        "alpha": str(c.alpha), "gw_hi_us": c.hi_us, "gl_us": gl_of[it]}
+                       for it, c in cal.items()]
+    if targets is not None:
+        out.note = f"target SM counts {[int(x) for x in targets]}"
     if not report.schedulable:
         out.note = "analysis rejects the calibrated task set; nothing to execute"
         return out
@@ -325,6 +378,7 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
             nxt += nxt % 2  # the next task starts on a fresh TPC
     if nxt > n_sm:
         raise ValueError(f"partitions need {nxt} SMs, the GPU has {n_sm}")
+    out.sms_used = sum(len(p) for p in parts)
     out.allocation = {s.id: alloc[s.id] for s in specs}
     # the executor arbitrates the bus and the CPU with the analysis' own
     # (deadline-monotonic) priorities, not the order tasks were drawn in

@@ -1,23 +1,42 @@
 """Executor robustness: measured WCRT / R_k and kernel span / GR_up over
-many seeds and utilisations (default host models).  Writes a JSON list."""
+many seeds and load levels.  One JSON line per run, then a summary line.
+
+    python scripts/wcrt_robustness.py [--wide] [--seeds N] [--horizon-s S]
+
+--wide: partitions of several to tens of SMs (wcrt_experiment width mode,
+three target-width ranges as the load levels); default: the utilisation
+mode (2.5 / 3.0 / 4.0)."""
+import argparse
 import json
 import sys
 
 sys.path.insert(0, ".")
 from paper_2101_10463_b200 import executor as ex  # noqa: E402
 
+ap = argparse.ArgumentParser()
+ap.add_argument("--wide", action="store_true")
+ap.add_argument("--seeds", type=int, default=8)
+ap.add_argument("--horizon-s", type=float, default=1.0)
+args = ap.parse_args()
+levels = [(4, 12), (12, 24), (24, 36)] if args.wide else [2.5, 3.0, 4.0]
 out = []
-for seed in range(1, 9):
-    for util in (2.5, 3.0, 4.0):
-        r = ex.wcrt_experiment(n_tasks=4, m=3, horizon_us=1.0e6, seed=seed, utilization=util)
-        rec = {"seed": seed, "util": util, "schedulable": r.schedulable,
+for seed in range(1, args.seeds + 1):
+    for lv in levels:
+        kw = dict(width=lv) if args.wide else dict(utilization=lv)
+        r = ex.wcrt_experiment(n_tasks=4, m=3, horizon_us=args.horizon_s * 1e6, seed=seed, **kw)
+        rec = {"seed": seed, "level": lv, "schedulable": r.schedulable,
                "max_wcrt_over_bound": round(r.max_ratio, 4),
                "max_kernel_span_over_lemma4": round(r.max_kernel_ratio, 4),
-               "all_within_bound": r.all_within_bound, "allocation": r.allocation}
+               "all_within_bound": r.all_within_bound, "kernels_within_bound": r.kernels_within_bound,
+               "allocation_vsm": r.allocation, "sms_used": r.sms_used,
+               "jobs": [t["jobs"] for t in r.tasks], "note": r.note}
         out.append(rec)
         print(json.dumps(rec), flush=True)
 ok = [x for x in out if x["schedulable"]]
-print(json.dumps({"runs": len(out), "schedulable": len(ok),
-                  "violations": sum(not x["all_within_bound"] for x in ok),
-                  "worst_wcrt_ratio": max(x["max_wcrt_over_bound"] for x in ok),
-                  "worst_kernel_ratio": max(x["max_kernel_span_over_lemma4"] for x in ok)}))
+print(json.dumps({"summary": True, "runs": len(out), "schedulable": len(ok),
+                  "jobs_over_bound_runs": sum(not x["all_within_bound"] for x in ok),
+                  "kernel_overrun_runs": sum(not x["kernels_within_bound"] for x in ok),
+                  "worst_wcrt_ratio": max((x["max_wcrt_over_bound"] for x in ok), default=None),
+                  "worst_kernel_ratio": max((x["max_kernel_span_over_lemma4"] for x in ok), default=None),
+                  "min_sms_used": min((x["sms_used"] for x in ok), default=None),
+                  "max_sms_used": max((x["sms_used"] for x in ok), default=None)}), flush=True)
