@@ -308,6 +308,13 @@ template <class V> struct Layout {
     }
 };
 
+/* view word WN: negative gaps of the chain (analysis.py:57, :89) */
+enum {
+    WN_WRAP = 1,          /* the steady-state wrap-around gap (checked: InfeasibleGapError) */
+    WN_FIRST_CHECKED = 2, /* the first job's deadline-side gap of a memory chain (checked) */
+    WN_FIRST_OPEN = 4     /* the first job's CPU gap T - D < 0 (used as is) */
+};
+
 /* view offsets inside one task's chain view */
 struct VOff {
     int e, P, EP, F1, WN, INV;
@@ -558,6 +565,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         v[o.INV] = Num<V>::make_inv(v[o.P + 1]);
         return;
     }
+    if (m == 0) return; /* no segments: no chain (walks need p >= 1) */
     /* CPU chain */
     {
         VOff o(c.MC);
@@ -583,7 +591,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         v[o.EP + m] = EP;
         v[o.F1] = P + elast + N::sc(t.T - t.D, q);
         V wrap = N::sc(t.T - t.sClu - t.sMll, q) - (t.isgpu ? (V)t.sGWlo * (V)perlo : (V)0);
-        v[o.WN] = wrap < 0 ? (V)1 : (V)0;
+        v[o.WN] = (wrap < 0 ? (V)WN_WRAP : (V)0) + (t.D > t.T ? (V)WN_FIRST_OPEN : (V)0);
         v[o.P + m] = P + elast + (wrap < 0 ? (V)0 : wrap);
         v[o.INV] = Num<V>::make_inv(v[o.P + m]);
         (void)g;
@@ -615,7 +623,7 @@ RT_NI void build_view(SetCtx<V> &c, int i, typename Num<V>::Qt q) {
         if (c.mm == RTGPU_ONE_COPY) first += (V)gw_lo[m - 2] * (V)perlo;
         v[o.F1] = P + elast + first;
         V wrap = N::sc(t.T - t.sMlu - t.innerCll, q) - (V)t.sGWlo * (V)perlo;
-        v[o.WN] = wrap < 0 ? (V)1 : (V)0;
+        v[o.WN] = (wrap < 0 ? (V)WN_WRAP : (V)0) + (first < 0 ? (V)WN_FIRST_CHECKED : (V)0);
         v[o.P + p] = P + elast + (wrap < 0 ? (V)0 : wrap);
         v[o.INV] = Num<V>::make_inv(v[o.P + p]);
     }
@@ -766,7 +774,21 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
     V base = P[h];
     V lim = H + base;
     V F1 = v[o.F1];
-    if (F1 > lim) {
+    const int fl = (int)v[o.WN];
+    bool in_first = F1 > lim;
+    if (fl & (WN_FIRST_CHECKED | WN_FIRST_OPEN)) {
+        /* a negative gap after the first job (D > T): the walk evaluates it
+         * once it reaches the job's last segment -- the memory chain's is
+         * checked (InfeasibleGapError), the CPU chain's used as is, so the
+         * walk leaves the first job only if it got there */
+        const bool reach_last = P[p - 1] <= lim;
+        if ((fl & WN_FIRST_CHECKED) && reach_last) {
+            err = true;
+            return 0;
+        }
+        if (!reach_last) in_first = true;
+    }
+    if (in_first) {
         /* stops inside the first (partial) job: the last x in [h, p-1] with
          * P[x] <= lim (P is non-decreasing; P[h] = base <= lim) */
         int x = h;
@@ -787,7 +809,7 @@ RT_HD V walk(const V *v, int PM, int half, int p, int h, V H, V &rho, bool &err)
     V H2 = lim - F1; /* H minus the first job's span */
     int x = 0;
     V Hs;
-    if (v[o.WN] != 0) {
+    if (fl & WN_WRAP) {
         /* negative wrap: the walk raises iff it reaches index 2p-1 */
         if (P[p - 1] <= H2) {
             err = true;
@@ -1106,7 +1128,13 @@ RT_NI void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
     t.isgpu = t.m > 1;
     const int m = t.m, p = t.p;
     int want_p = m < 2 ? 0 : (c.mm == RTGPU_TWO_COPY ? 2 * m - 2 : m - 1);
-    if (m < 1 || m > c.MC || p != want_p || p > c.MP || t.T <= 0 || t.D <= 0 || t.D > t.T) {
+    /* m == 0 (no segments) and D > T are analysed as the reference does
+     * without validate_taskset: a task with no segments has bound 0 and no
+     * workload; D > T makes the first job's CPU gap T - D negative (used as
+     * is, analysis.py:100) and its memory deadline-side gap checked
+     * (analysis.py:75: InfeasibleGapError when a walk reaches it), so such
+     * sets take the exact depth-first search (TF_IRREG) */
+    if (m < 0 || m > c.MC || p != want_p || p > c.MP || t.T <= 0 || t.D <= 0) {
         t.flags |= TF_UNSUP;
         *vb_out = 0;
         return;
@@ -1176,6 +1204,7 @@ RT_NI void load_task(SetCtx<V> &c, int i, i128 *vb_out) {
         if (t.sClu > t.D) t.flags |= TF_ISOFAIL;
         if (t.T - t.sClu < 0) t.flags |= TF_IRREG;
     }
+    if (t.D > t.T) t.flags |= TF_IRREG;
 }
 
 /* ------------------------------------------------------------ output helpers */
@@ -1475,6 +1504,7 @@ template <class V> RT_HD bool susp_valid(const SetCtx<V> &c, const TaskRec &t, i
     typename Num<V>::Qt perlo = t.isgpu ? q / (2 * (typename Num<V>::Qt)gcount) : q;
     typename Num<V>::Qt perhi =
         t.isgpu ? q / ((typename Num<V>::Qt)2 * (typename Num<V>::Qt)c.A * gcount) : q;
+    if (t.D > t.T) return false; /* SuspTask: 0 < D <= T (suspension.py:40) */
     auto grl = [&](int j) { return (V)gw_lo[j] * (V)perlo; };
     auto gru = [&](int j) {
         return (V)((i128)gw_hi[j] * an[j] - (i128)gl[j] * c.A) * (V)perhi + Num<V>::sc(gl[j], q);
@@ -1488,6 +1518,7 @@ template <class V> RT_HD bool susp_valid(const SetCtx<V> &c, const TaskRec &t, i
         }
         return lo <= hi && hi <= Num<V>::sc(t.T, q);
     }
+    if (m < 1) return false; /* SuspTask: at least one execution segment */
     #pragma unroll 1
     for (int j = 0; j < m; j++)
         if (cl_lo[j] > cl_hi[j]) return false;

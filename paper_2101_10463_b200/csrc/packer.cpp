@@ -197,8 +197,8 @@ bool read_task(PyObject *t, TaskF &r, int mem_model) {
     Py_DECREF(gpu);
     if (!ok) return false;
     /* pack._check_shape */
-    if (m < 1 || m > 16) return fail("engine supports 1..16 CPU segments");
-    if (g != m - 1) return fail("gpu segment count != m - 1");
+    if (m < 0 || m > 16) return fail("engine supports 0..16 CPU segments");
+    if (g != (m > 0 ? m - 1 : 0)) return fail("gpu segment count != m - 1");
     const Py_ssize_t want = m < 2 ? 0 : (mem_model == 0 ? 2 * m - 2 : m - 1);
     if (pn != want) return fail("mem segment count mismatch");
     return true;
@@ -295,7 +295,7 @@ bool pack_one(PyObject *ts, std::vector<int64_t> &words, int64_t &scale, std::ve
             !put(t.gl))
             return false;
         for (const Frac &ra : t.ratio) words.push_back(ra.n * (A / ra.d));
-        seg_off += 2 * m + 2 * p + 4 * (m - 1);
+        seg_off += 2 * m + 2 * p + 4 * (m > 0 ? m - 1 : 0);
     }
     words[base + 4] = (int64_t)(words.size() - base);
     scale = S;

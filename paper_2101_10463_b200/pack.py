@@ -98,10 +98,10 @@ def _check_shape(ts: TaskSet) -> None:
         raise ValueError(f"engine supports at most {MAX_TASKS} tasks per set")
     for t in ts.tasks:
         m = len(t.cpu_segments)
-        if not 1 <= m <= MAX_M:
-            raise ValueError(f"task {t.id}: engine supports 1..{MAX_M} CPU segments")
-        if len(t.gpu_segments) != m - 1:
-            raise ValueError(f"task {t.id}: gpu segment count != {m - 1}")
+        if not 0 <= m <= MAX_M:
+            raise ValueError(f"task {t.id}: engine supports 0..{MAX_M} CPU segments")
+        if len(t.gpu_segments) != max(m - 1, 0):
+            raise ValueError(f"task {t.id}: gpu segment count != {max(m - 1, 0)}")
         want = expected_mem_count(m, ts.mem_model)
         if len(t.mem_segments) != want:
             raise ValueError(f"task {t.id}: mem segment count != {want}")
@@ -291,7 +291,7 @@ def unpack_report(batch: PackedBatch, res: RawResults, s: int,
             rec = batch.blobs[meta.word_off + HDR_WORDS + TASK_WORDS * i:
                               meta.word_off + HDR_WORDS + TASK_WORDS * (i + 1)]
             m, p = int(rec[0]), int(rec[1])
-            g = m - 1
+            g = max(m - 1, 0)
             base = meta.word_off + int(rec[5])
             d = res.detail[base: base + 2 * m + 2 * p + 4 * g]
             gl = d[2 * m + 2 * p: 2 * m + 2 * p + g]
