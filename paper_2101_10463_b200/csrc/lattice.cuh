@@ -430,7 +430,7 @@ RT_HD void lat_slot(const LChains &ch, double bN, i64 bf, i64 d, double invd, in
 #ifdef __CUDACC__
 template <int W>
 __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &ch, double bN, i64 bf, i64 d,
-                                             double invd, LCache &cache) {
+                                             double invd, LCache &cache, bool jump = true) {
     LatAcc a = {0.0, 0.0, false};
     const int per = 32 >> ch.lg, G = 1 << ch.lg;
     const int R = (ch.k + per - 1) / per;
@@ -452,7 +452,7 @@ __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &
             }
         }
         lat_group(bw, s, invs, phv, a); /* every lane of the group holds its task's sums */
-        a.f += br;
+        if (jump) a.f += br;
     }
     /* butterfly sums over the groups: identical on every lane (IEEE
      * addition commutes), so the team takes one decision */
@@ -483,7 +483,8 @@ __device__ __forceinline__ LatAcc lat_interf(const LTeam<W> &tm, const LChains &
 }
 #endif
 
-RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 d, double invd, LCache *cache) {
+RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 d, double invd, LCache *cache,
+                        bool jump = true) {
     LatAcc a = {0.0, 0.0, false};
     const int per = 32 >> ch.lg, G = 1 << ch.lg;
 #ifdef RTGPU_LAT_NOCACHE
@@ -503,7 +504,7 @@ RT_HD LatAcc lat_interf(const LSeq &, const LChains &ch, double bN, i64 bf, i64 
                 }
             }
             lat_group(m, s, invs, phv, a);
-            a.f += rm;
+            if (jump) a.f += rm;
         }
     return a;
 }
@@ -525,12 +526,23 @@ RT_HD double lat_rcp(i64 d) {
  * N (a lower bound of N*).  -1 = None (suspension.py:123: beyond D),
  * -2 = iteration cap. */
 template <class TM>
-RT_NI double lfp_lat(const TM &tm, const LChains ch, const LBase b, double N, i64 D) {
+RT_NI double lfp_lat(const TM &tm, const LChains ch, const LBase b, double N, i64 D, int mode = 0) {
     RT_COUNT(g_cnt_flfp[ch.res]);
     if (lb_over(b, N, D)) return -1.0;
     const double invd = b.bf ? lat_rcp(b.d) : 0.0;
     typename TM::Cache cache;
     tm.cache_reset(cache);
+    if (mode == 1) {
+        /* Is b + N a pre-fixed point?  f(r) <= r with r = b + N puts the lfp
+         * at or below r (and then, f being monotone, at or below f(r)):
+         * return floor(I(r)), the offset of f(r) rounded down to the
+         * lattice, or -1 when not verified.  I(r) = q + F, F the exact sum
+         * of the fractional parts (FP64 a.f within 1e-9 of it). */
+        RT_COUNT(g_cnt_fit[ch.res]);
+        const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd, tm.cache_ptr(cache), false);
+        const double ub = floor(a.q + a.f + 1e-6);
+        return (a.q + a.f + 1e-6 <= N) ? ub : -1.0;
+    }
     #pragma unroll 1
     for (int it = 0; it < ITER_CAP; it++) {
         RT_COUNT(g_cnt_fit[ch.res]);
@@ -940,6 +952,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
      * valid for any later task (hp(k) only grows) at a base >= its base */
     LBase mw = {-1, 0, 1}, cw = {-1, 0, 1};
     double mwN = 0, cwN = 0;
+    double mg = -1.0; /* the last task's memory offset (or its verified bound): the next guess */
     int st = RTGPU_SCHEDULABLE;
     const int W = tm.width();
     #pragma unroll 1
@@ -964,24 +977,42 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
             glo = gm;
             ghi = (int)gmax;
         }
-        /* ---- g-independent: the longest copy's response bounds every MR */
-        i64 mr_ub = 0, sum_mr = -1;
+        /* ---- g-independent: the longest copy's response bounds every MR.
+         * First a guess verified in one evaluation: the previous task's
+         * offset grown by half, accepted when b + N is a pre-fixed point
+         * (then lfp <= f(b + N) <= D: every MR exists and MR_j <= the bound
+         * minus (bmax - b_j)); consecutive tasks' memory fixed points differ
+         * by ~14% (hp(k) grows by one task), so the guess usually holds and
+         * saves the iterations from 0.  The exact fixed point is computed
+         * only if R2 fails with the looser bound. */
+        i64 mr_ub = 0, sum_mr = -1, bsum = 0;
+        LBase lbm = {0, 0, 1};
+        bool rmax_exact = true;
         if (p > 0) {
-            i64 bmax = 0, bsum = 0;
+            i64 bmax = 0;
             #pragma unroll 1
             for (int j = 0; j < p; j++) {
                 bmax = tmax(bmax, (i64)ml_hi[j] + B);
                 bsum += ml_hi[j] + B;
             }
-            const LBase lb = {bmax, 0, 1};
-            const double r = lfp_lat(tm, chm, lb, (mw.bi >= 0 && lb_le(mw, lb)) ? mwN : 0.0, D);
-            if (r == -2.0) return ST_ESCALATE;
-            if (r < 0) {
-                st = RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None at every count */
-                break;
+            lbm = {bmax, 0, 1};
+            double r = -1.0;
+            if (mg >= 1.0) { /* (after a task without memory interference there is nothing to grow) */
+                const double Ng = ceil(1.5 * mg) + 1.0;
+                if (!lb_over(lbm, Ng, D)) r = lfp_lat(tm, chm, lbm, Ng, D, 1);
+                rmax_exact = r < 0;
             }
-            mw = lb;
-            mwN = r;
+            if (r < 0) {
+                r = lfp_lat(tm, chm, lbm, (mw.bi >= 0 && lb_le(mw, lbm)) ? mwN : 0.0, D);
+                if (r == -2.0) return ST_ESCALATE;
+                if (r < 0) {
+                    st = RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None at every count */
+                    break;
+                }
+                mw = lbm;
+                mwN = r;
+            }
+            mg = r;
             mr_ub = (i64)p * (i64)r + bsum;
         } else {
             sum_mr = 0;
@@ -999,6 +1030,22 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                     smr = p > 0 ? mr_ub : 0;
                 } else {
                     if (p == 0) break;
+                    if (!rmax_exact) {
+                        /* the verified guess was too loose for R2: the exact
+                         * fixed point of the longest copy, then R2 again */
+                        const double r = lfp_lat(tm, chm, lbm, 0.0, D);
+                        if (r < 0) return -1; /* cannot be None below a verified bound */
+                        rmax_exact = true;
+                        mw = lbm;
+                        mwN = r;
+                        mg = r;
+                        const i64 ub = (i64)p * (i64)r + bsum;
+                        if (ub < mr_ub) {
+                            mr_ub = ub;
+                            pass = -1; /* retry R2 with the exact bound */
+                            continue;
+                        }
+                    }
                     if (sum_mr < 0) {
                         tm.pfor(p, [&](int j) { c.bases()[j] = ml_hi[j] + B; });
                         sum_mr = lat_chain_sum(tm, c, chm, p, D);

@@ -18,7 +18,7 @@ ap.add_argument("--wide", action="store_true")
 ap.add_argument("--seeds", type=int, default=8)
 ap.add_argument("--horizon-s", type=float, default=1.0)
 args = ap.parse_args()
-levels = [(4, 12), (12, 24), (24, 36)] if args.wide else [2.5, 3.0, 4.0]
+levels = [(8, 16), (16, 28), (28, 40)] if args.wide else [2.5, 3.0, 4.0]
 out = []
 for seed in range(1, args.seeds + 1):
     for lv in levels:
