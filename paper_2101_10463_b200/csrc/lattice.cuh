@@ -1055,6 +1055,11 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                     smr = sum_mr;
                 }
                 const LBase b = {gr.bi + smr + sClu, gr.bf, gr.d};
+                /* R2 passes iff lfp <= D; a pre-fixed point at the deadline
+                 * itself (f(D) <= D) proves it in one evaluation -- the
+                 * common case with slack; otherwise the fixed point */
+                const double nd = (double)(D - b.bi - (b.bf > 0 ? 1 : 0));
+                if (nd >= 0 && lfp_lat(tm, chc, b, nd, D, 1) >= 0) return 1;
                 const double r = lfp_lat(tm, chc, b, (cw.bi >= 0 && lb_le(cw, b)) ? cwN : 0.0, D);
                 if (r == -2.0) return -1;
                 if (r >= 0) {
