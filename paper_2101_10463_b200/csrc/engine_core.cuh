@@ -1892,8 +1892,11 @@ RT_NI void load_task_fast_s(const i64 *blob, unsigned char *hbase, int o_tr, int
 /* least fixed point on a fixed scale; -1 = None, -2 = iteration cap */
 template <class V, class TM>
 RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kind, int lg,
-                 int PM, int half, int stride, V base, V start, V bound) {
-    if (base > bound || start > bound) return (V)-1; /* start: a lower bound of the lfp */
+                 int PM, int half, int stride, V base, V start, V bound, int check = 0) {
+    /* check = 1: is `start` a pre-fixed point (base + I(start) <= start)?
+     * Then the lfp is at most f(start), which is returned; else -3.
+     * Otherwise `start` is a lower bound of the lfp. */
+    if (base > bound || start > bound) return (V)-1;
     RT_COUNT(g_cnt_flfp[kind]);
     V r = start;
     for (int it = 0; it < ITER_CAP; it++) {
@@ -1919,6 +1922,7 @@ RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kin
         tm.acc_sum(lg, acc, I, err);
         if (err) return (V)-1;
         V nxt = base + I;
+        if (check) return nxt <= r ? nxt : (V)-3;
         if (nxt <= r) return r;
         nxt += tm.acc_rho(acc);
         if (nxt > bound) return (V)-1;
@@ -2014,6 +2018,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     if (lg_tab) tm.pfor(gtop, [&](int x) { outs[x] = (V)(L / (Qt)(x + 1)); });
     i64 used = 0, rest_min = need;
     V mem_prev_b = -1, mem_prev_r = 0; /* last memory fixed point (base, value) */
+    V mem_guess = 0;                   /* last memory offset (or verified bound): the next guess */
     #pragma unroll 1
     for (int k = 0; k < n; k++) {
         const TaskRec &t = tr[k];
@@ -2038,7 +2043,9 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         }
         /* ---- g-independent part: memory responses (Lemma 6) */
         V sum_mr = 0, mr_ub = 0;
-        bool have_exact_mr = t.p == 0;
+        bool have_exact_mr = t.p == 0, rmax_exact = true;
+        i64 bsum_k = 0;
+        V bmax_k = 0;
         if (t.p > 0) {
             i64 bmax_t = 0, bsum_t = 0;
             #pragma unroll 1
@@ -2047,18 +2054,33 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                 bsum_t += ml_hi[j] + t.B;
             }
             const V bmax = Num<V>::sc(bmax_t, q);
+            bsum_k = bsum_t;
+            bmax_k = bmax;
             /* warm start across tasks: hp(k) grows with k, so the memory
              * interference of task k is pointwise >= that of any earlier
              * task, and lfp(b') >= lfp(b) + (b' - b) for b' >= b: the
              * previous task's fixed point shifted by the base difference is
              * below this one */
-            V start = bmax;
-            if (mem_prev_b >= 0 && bmax >= mem_prev_b) start = tmax(bmax, mem_prev_r + (bmax - mem_prev_b));
-            const V rmax = start > D ? (V)-1 : lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, start, D);
-            if (rmax == (V)-2) return ST_ESCALATE;
-            if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
-            mem_prev_b = bmax;
-            mem_prev_r = rmax;
+            V rmax = -1;
+            if (mem_guess > 0) {
+                /* the previous task's memory offset grown by half, verified
+                 * as a pre-fixed point in one evaluation (then the lfp is at
+                 * most f(U) <= D: every MR exists, bounded via f(U)); the
+                 * exact fixed point only if R2 needs it (lattice.cuh) */
+                const V U = bmax + Num<V>::sc(1, q) + floor(mem_guess * 1.5);
+                if (U <= D) rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, U, D, 1);
+                rmax_exact = rmax < 0;
+            }
+            if (rmax < 0) {
+                V start = bmax;
+                if (mem_prev_b >= 0 && bmax >= mem_prev_b) start = tmax(bmax, mem_prev_r + (bmax - mem_prev_b));
+                rmax = start > D ? (V)-1 : lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, start, D);
+                if (rmax == (V)-2) return ST_ESCALATE;
+                if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
+                mem_prev_b = bmax;
+                mem_prev_r = rmax;
+            }
+            mem_guess = rmax - bmax;
             mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
         }
         V sum_cr = -1; /* not computed yet; -2: some CR is None */
@@ -2070,7 +2092,21 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                                    : (V)0;
             const V cl = Num<V>::sc(t.sClu, q);
             if (t.p > 0 || !have_exact_mr) {
-                const V b2 = grup + mr_ub + cl;
+                V b2 = grup + mr_ub + cl;
+                /* R2 proven at the deadline itself (f(D) <= D) in one evaluation */
+                if (b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0) return 1;
+                if (!rmax_exact) {
+                    /* the verified memory bound was loose: the exact one */
+                    const V rm = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax_k, bmax_k, D);
+                    if (rm < 0) return -1; /* cannot be None below a verified bound */
+                    rmax_exact = true;
+                    mem_prev_b = bmax_k;
+                    mem_prev_r = rm;
+                    mem_guess = rm - bmax_k;
+                    mr_ub = (V)t.p * (rm - bmax_k) + Num<V>::sc(bsum_k, q);
+                    b2 = grup + mr_ub + cl;
+                    if (b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0) return 1;
+                }
                 const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
                 if (r == (V)-2) return -1;
                 if (r >= 0) return 1;
@@ -2106,6 +2142,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                 }
             } else {
                 const V b3 = grup + cl;
+                if (b3 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, D, D, 1) >= 0) return 1;
                 const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
                 if (r3 == (V)-2) return -1;
                 if (r3 >= 0) return 1;

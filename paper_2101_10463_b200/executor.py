@@ -201,6 +201,7 @@ def _ceil_margin(x_us: float, margin: float) -> int:
 
 
 CAL_SMS = (0, 74)  # one SM on each die: L2 distance differs per die
+_CAL_CACHE: dict = {}
 
 
 # Safety margin on measured worst cases.  A kernel's speed on its SMs depends
@@ -297,16 +298,23 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
     defs = []
     items_rng = (400, 3000) if width is None else (6000, 20000)
     for i in range(n_tasks):
+        items = rng.integers(*items_rng, m - 1)
+        if width is not None:
+            items = (items // 2000) * 2000  # a few sizes: calibrations are reused across runs
         defs.append(ExecTaskDef(
             cpu_us=[int(x) for x in rng.integers(100, 600, m)],
             copy_bytes=[int(x) for x in rng.integers(1 << 18, 4 << 20, 2 * m - 2)],
-            kernel_items=[int(x) for x in rng.integers(*items_rng, m - 1)]))
-    # calibrate every kernel and copy on the device
+            kernel_items=[int(x) for x in items]))
+    # calibrate every kernel and copy on the device (kept per process: the
+    # same kernel size is not re-timed by the next experiment)
     cal = {}
     for d in defs:
         for it in d.kernel_items:
             if it not in cal:
-                cal[it] = calibrate_kernel(it, iters, margin=margin)
+                key = (it, iters, margin)
+                if key not in _CAL_CACHE:
+                    _CAL_CACHE[key] = calibrate_kernel(it, iters, margin=margin)
+                cal[it] = _CAL_CACHE[key]
     # critical-path overhead GL: host wall time of an empty launch (what the
     # job path adds around every kernel), worst of many
     overhead = max(launch_us(list(range(8)), 50) +

@@ -108,13 +108,24 @@ def launches(path):
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    tag = sys.argv[sys.argv.index("--tag") + 1] if "--tag" in sys.argv else "r1"
-    args = [a for a in args if a != tag]
+    """python scripts/make_profiles.py REP [LAUNCHES.csv] --tag T [--key fast_kernel]
+    [--sets N] [--lib-sha SHA]: the capture's summary is merged into
+    profiles/ncu_summary.json under kernels[key] (bench.py reads it and checks
+    lib_sha against the library it benches)."""
+    argv = sys.argv[1:]
+    opt = {}
+    for name in ("--tag", "--key", "--sets", "--lib-sha"):
+        if name in argv:
+            i = argv.index(name)
+            opt[name] = argv[i + 1]
+            del argv[i:i + 2]
+    args = [a for a in argv if not a.startswith("--")]
+    tag = opt.get("--tag", "r1")
+    key = opt.get("--key", "fast_kernel")
     rep = args[0]
     os.makedirs(PROF, exist_ok=True)
     s = summarise(rep)
-    with open(os.path.join(PROF, f"{tag}_front_kernel.json"), "w") as fh:
+    with open(os.path.join(PROF, f"{tag}_{key}.json"), "w") as fh:
         json.dump(s, fh, indent=1)
     launch = None
     if len(args) > 1 and os.path.exists(args[1]):
@@ -123,23 +134,41 @@ def main():
         with open(os.path.join(PROF, f"{tag}_launch_shares.json"), "w") as fh:
             json.dump(launch, fh, indent=1)
     traffic = (s.get("dram_read_bytes") or 0) + (s.get("dram_write_bytes") or 0)
-    summary = {
+    entry = {
         "source": os.path.basename(rep),
+        "tag": tag,
         "kernel": s["kernel"],
+        "duration_ns": s.get("duration_ns"),
         "dram_bytes_per_launch": traffic,
+        "dram_read_bytes": s.get("dram_read_bytes"),
+        "dram_write_bytes": s.get("dram_write_bytes"),
+        "warp_instructions": s.get("warp_instructions"),
+        "lib_sha": opt.get("--lib-sha"),
         "issue": {"ipc_active": s.get("ipc_active"), "issue_slots_busy_pct": s.get("issue_active_pct"),
                   "peak_ipc": 4.0, "fp64_pipe_pct": s.get("fp64_pipe_pct"),
                   "alu_pipe_pct": s.get("alu_pipe_pct"), "fma_pipe_pct": s.get("fma_pipe_pct"),
                   "lsu_pipe_pct": s.get("lsu_pipe_pct"),
                   "achieved_occupancy_pct": s.get("achieved_occupancy_pct"),
+                  "registers_per_thread": s.get("registers_per_thread"),
                   "active_threads_per_warp_inst": s.get("active_threads_per_warp_inst"),
                   "branch_uniform_pct": s.get("branch_uniform_pct"),
-                  "top_stalls": s["stall_share"], "source": f"ncu {os.path.basename(rep)}"},
+                  "top_stalls": s["stall_share"]},
         "launch_shares": launch,
     }
-    with open(os.path.join(PROF, "ncu_summary.json"), "w") as fh:
+    if "--sets" in opt and s.get("warp_instructions"):
+        entry["sets_per_launch"] = int(opt["--sets"])
+        entry["warp_instructions_per_set"] = s["warp_instructions"] / int(opt["--sets"])
+    path = os.path.join(PROF, "ncu_summary.json")
+    summary = {}
+    if os.path.exists(path):
+        with open(path) as fh:
+            summary = json.load(fh)
+    if "kernels" not in summary:
+        summary = {"kernels": {}}
+    summary["kernels"][key] = entry
+    with open(path, "w") as fh:
         json.dump(summary, fh, indent=1)
-    print(json.dumps(summary, indent=1))
+    print(json.dumps(entry, indent=1))
 
 
 if __name__ == "__main__":
