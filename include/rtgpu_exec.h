@@ -15,7 +15,9 @@ extern "C" {
 #endif
 
 #define RTGPU_EXEC_MASK_WORDS 8    /* SM bitmap: up to 256 SMs            */
+#ifndef RTGPU_EXEC_BLOCKS_PER_SM
 #define RTGPU_EXEC_BLOCKS_PER_SM 6 /* launch width per SM (>= 2 slots)    */
+#endif
 
 typedef struct {
     int32_t m;                    /* CPU segments                              */

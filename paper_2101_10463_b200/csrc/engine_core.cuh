@@ -1931,6 +1931,10 @@ RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kin
     return (V)-2;
 }
 
+#ifndef RTGPU_FAST_DCHECK
+#define RTGPU_FAST_DCHECK 1 /* A/B builds: 0 turns off the deadline pre-fixed-point check */
+#endif
+
 /* ST_ESCALATE_RANGE: only the scale did not fit V (the int64 instance may) */
 enum { ST_ESCALATE_RANGE = 98 };
 
@@ -2062,7 +2066,14 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
              * previous task's fixed point shifted by the base difference is
              * below this one */
             V rmax = -1;
+            /* off by default: on the 8 x 5 benchmark the longer code costs more
+             * than the saved iterations (scripts/gpu_lat_ab.sh r2l: 24.4 vs
+             * 25.5 M sets/s); the lattice path keeps it (alloc64 +14%) */
+#ifdef RTGPU_FAST_GUESS
             if (mem_guess > 0) {
+#else
+            if (false) {
+#endif
                 /* the previous task's memory offset grown by half, verified
                  * as a pre-fixed point in one evaluation (then the lfp is at
                  * most f(U) <= D: every MR exists, bounded via f(U)); the
@@ -2094,7 +2105,8 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
             if (t.p > 0 || !have_exact_mr) {
                 V b2 = grup + mr_ub + cl;
                 /* R2 proven at the deadline itself (f(D) <= D) in one evaluation */
-                if (b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0) return 1;
+                if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
+                    return 1;
                 if (!rmax_exact) {
                     /* the verified memory bound was loose: the exact one */
                     const V rm = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax_k, bmax_k, D);
@@ -2105,7 +2117,8 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                     mem_guess = rm - bmax_k;
                     mr_ub = (V)t.p * (rm - bmax_k) + Num<V>::sc(bsum_k, q);
                     b2 = grup + mr_ub + cl;
-                    if (b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0) return 1;
+                    if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
+                        return 1;
                 }
                 const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
                 if (r == (V)-2) return -1;
@@ -2142,7 +2155,8 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                 }
             } else {
                 const V b3 = grup + cl;
-                if (b3 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, D, D, 1) >= 0) return 1;
+                if (RTGPU_FAST_DCHECK && b3 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, D, D, 1) >= 0)
+                    return 1;
                 const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
                 if (r3 == (V)-2) return -1;
                 if (r3 >= 0) return 1;

@@ -312,6 +312,26 @@ RT_HD int lat_lg(int k, int PM, int W) {
     return lg;
 }
 
+/* What an out-of-line fixed point is handed (a few words, no set context):
+ * where the slab is, the batch dims, the task and the resource; the chain
+ * geometry is rebuilt from them inside. */
+struct LKey {
+    unsigned char *hbase; /* host harness only */
+    int base, maxn, MC, MP, task, res;
+};
+
+RT_HD LKey lat_key(const LCtx &c, int k, int res) {
+    LKey q;
+    q.hbase = c.hbase;
+    q.base = c.base;
+    q.maxn = c.L.maxn;
+    q.MC = c.L.MC;
+    q.MP = c.L.MP;
+    q.task = k;
+    q.res = res;
+    return q;
+}
+
 RT_HD LChains lat_chains(const LCtx &c, int k, int res, int W) {
     LChains ch;
     ch.hbase = c.hbase;
@@ -526,7 +546,12 @@ RT_HD double lat_rcp(i64 d) {
  * N (a lower bound of N*).  -1 = None (suspension.py:123: beyond D),
  * -2 = iteration cap. */
 template <class TM>
-RT_NI double lfp_lat(const TM &tm, const LChains ch, const LBase b, double N, i64 D, int mode = 0) {
+RT_NI double lfp_lat(const TM &tm, const LKey key, const LBase b, double N, i64 D, int mode = 0) {
+    LCtx c;
+    c.hbase = key.hbase;
+    c.base = key.base;
+    c.L.init(Dims{key.maxn, key.MC, key.MP});
+    const LChains ch = lat_chains(c, key.task, key.res, tm.width());
     RT_COUNT(g_cnt_flfp[ch.res]);
     if (lb_over(b, N, D)) return -1.0;
     const double invd = b.bf ? lat_rcp(b.d) : 0.0;
@@ -771,7 +796,7 @@ RT_HD void lat_view(const LSeq &, const LCtx &c, int i) {
  * first None makes every larger base None.  Returns the sum, -1 (some None)
  * or -2 (iteration cap). */
 template <class TM>
-RT_HD i64 lat_chain_sum(const TM &tm, const LCtx &c, const LChains &ch, int cnt, i64 D) {
+RT_HD i64 lat_chain_sum(const TM &tm, const LCtx &c, const LKey &key, int cnt, i64 D) {
     i64 *bases = c.bases();
     int *ord = c.ord();
     tm.pfor(cnt, [&](int j) {
@@ -785,7 +810,7 @@ RT_HD i64 lat_chain_sum(const TM &tm, const LCtx &c, const LChains &ch, int cnt,
     #pragma unroll 1
     for (int st = 0; st < cnt; st++) {
         const i64 b = bases[ord[st]];
-        const double r = lfp_lat(tm, ch, LBase{b, 0, 1}, N, D);
+        const double r = lfp_lat(tm, key, LBase{b, 0, 1}, N, D);
         if (r < 0) {
             sum = r == -2.0 ? -2 : -1;
             break;
@@ -836,11 +861,11 @@ RT_HD int lat_report(const TM &tm, const LCtx &c, int have_views, bool stop_at_f
         if (p > 0) { /* analysis.py:156, every copy */
             const i64 B = c.B()[k];
             tm.pfor(p, [&](int j) { bases[j] = ml_hi[j] + B; });
-            sum_mr = lat_chain_sum(tm, c, lat_chains(c, k, K_MEM, tm.width()), p, D);
+            sum_mr = lat_chain_sum(tm, c, lat_key(c, k, K_MEM), p, D);
             if (sum_mr == -2) return ST_ESCALATE;
         }
         tm.pfor(m, [&](int j) { bases[j] = cl_hi[j]; });
-        const LChains chc = lat_chains(c, k, K_CPU, tm.width());
+        const LKey chc = lat_key(c, k, K_CPU);
         const i64 sum_cr = lat_chain_sum(tm, c, chc, m, D); /* analysis.py:175 */
         if (sum_cr == -2) return ST_ESCALATE;
         /* end_to_end (analysis.py:191): None if some MR is None; R1 if every
@@ -964,7 +989,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         const i64 D = c.D()[k], B = c.B()[k], sClu = c.sClu()[k];
         const Seg32 sg = c.segs(k);
         const Seg32 cl_hi = sg + m, ml_hi = sg + 2 * m + p;
-        const LChains chc = lat_chains(c, k, K_CPU, W), chm = lat_chains(c, k, K_MEM, W);
+        const LKey chc = lat_key(c, k, K_CPU), chm = lat_key(c, k, K_MEM);
         int glo = 0, ghi = 0;
         if (gpu) {
             const int gm = c.gmin()[k];
@@ -997,7 +1022,11 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
             }
             lbm = {bmax, 0, 1};
             double r = -1.0;
+#ifndef RTGPU_LAT_NOGUESS
             if (mg >= 1.0) { /* (after a task without memory interference there is nothing to grow) */
+#else
+            if (false) {
+#endif
                 const double Ng = ceil(1.5 * mg) + 1.0;
                 if (!lb_over(lbm, Ng, D)) r = lfp_lat(tm, chm, lbm, Ng, D, 1);
                 rmax_exact = r < 0;
@@ -1059,7 +1088,11 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                  * itself (f(D) <= D) proves it in one evaluation -- the
                  * common case with slack; otherwise the fixed point */
                 const double nd = (double)(D - b.bi - (b.bf > 0 ? 1 : 0));
+#ifndef RTGPU_LAT_NODCHECK
                 if (nd >= 0 && lfp_lat(tm, chc, b, nd, D, 1) >= 0) return 1;
+#else
+                (void)nd;
+#endif
                 const double r = lfp_lat(tm, chc, b, (cw.bi >= 0 && lb_le(cw, b)) ? cwN : 0.0, D);
                 if (r == -2.0) return -1;
                 if (r >= 0) {

@@ -29,7 +29,10 @@ for seed in range(1, args.seeds + 1):
                "max_kernel_span_over_lemma4": round(r.max_kernel_ratio, 4),
                "all_within_bound": r.all_within_bound, "kernels_within_bound": r.kernels_within_bound,
                "allocation_vsm": r.allocation, "sms_used": r.sms_used,
-               "jobs": [t["jobs"] for t in r.tasks], "note": r.note}
+               "jobs": [t["jobs"] for t in r.tasks], "note": r.note,
+               "blocks_per_launch_vs_2g": [(t["blocks_per_launch"], 2 * t["sms"]) for t in r.tasks],
+               "kernel_span_vs_gr_up": [t["kernel_span_us_vs_gr_up"] for t in r.tasks],
+               "worst_launch": [t["worst_launch"] for t in r.tasks]}
         out.append(rec)
         print(json.dumps(rec), flush=True)
 ok = [x for x in out if x["schedulable"]]

@@ -51,7 +51,8 @@ def test_wide_partitions_within_bounds(seed, width):
     from paper_2101_10463_b200 import executor as ex
     rep = ex.wcrt_experiment(n_tasks=4, m=3, horizon_us=1.0e6, seed=seed, width=width)
     assert rep.schedulable, rep.note
-    detail = [(t["task"], t["sms"], t["ratio"], t["kernel_span_us_vs_gr_up"]) for t in rep.tasks]
+    detail = [(t["task"], t["sms"], t["ratio"], t["kernel_span_us_vs_gr_up"], t["blocks_per_launch"],
+               t["worst_launch"]) for t in rep.tasks]
     assert min(t["sms"] for t in rep.tasks) >= 4, detail
     assert rep.all_within_bound, detail
     assert rep.kernels_within_bound and rep.max_kernel_ratio <= 1.0, detail
