@@ -915,390 +915,6 @@ RT_HD int lat_report(const TM &tm, const LCtx &c, int have_views, bool stop_at_f
     return 0;
 }
 
-/* The allocation search of lattice_set (greedy descent over counts, task by
- * task in priority order) as a state machine with ONE fixed-point call site:
- * every fixed point -- the longest copy's (guessed bound, then exact), R2
- * (checked at the deadline, then solved), the exact memory and CPU segment
- * chains for R1 -- is a request (resource, base, start, mode) the loop
- * issues at the bottom.  Out-of-line calls from many sites made the search
- * keep its state across the calling convention (spills, a large stack
- * frame) and grew the code past the instruction cache; here the state is
- * plain loop variables around one call.  Same decisions as the nested
- * version (RTGPU_LAT_LOOPS builds it, for A/B). */
-template <class TM>
-RT_HD int lat_search(const TM &tm, LCtx &c, i64 need, i64 &evals) {
-    enum {
-        S_TASK,      /* start task k */
-        S_MEMG,      /* consume: the verified guess of the longest copy's bound */
-        S_MEMX,      /* consume: the exact fixed point of the longest copy */
-        S_SEARCH,    /* start the count search of task k */
-        S_PASS,      /* start evaluating count `cand` */
-        S_R2,        /* issue R2 for the current sum-MR term */
-        S_R2CHK,     /* consume: R2 pre-fixed point at D */
-        S_R2LFP,     /* consume: R2 fixed point */
-        S_NEXTR2,    /* the R2 attempts after the first */
-        S_RMAX2,     /* consume: exact longest copy after a loose guess */
-        S_CHAIN,     /* issue the next fixed point of a chain */
-        S_CHAINR,    /* consume: one chain fixed point */
-        S_R1,        /* R1 with the CPU chain */
-        S_RESULT     /* the count search step with pass result `o` */
-    };
-    const int n = c.n, GN = c.GN;
-    const int *info = c.info();
-    i64 used = 0, rest_min = need;
-    LBase mw = {-1, 0, 1}, cw = {-1, 0, 1};
-    double mwN = 0, cwN = 0, mg = -1.0;
-    int k = 0, m = 0, p = 0;
-    bool gpu = false;
-    i64 D = 0, B = 0, sClu = 0;
-    int glo = 0, ghi = 0, lo = 0, hi = 0, cand = 0, sphase = 0;
-    i64 mr_ub = 0, sum_mr = -1, bsum = 0, sum_cr = -3;
-    LBase lbm = {0, 0, 1}, gr = {0, 0, 1}, b2 = {0, 0, 1};
-    bool rmax_exact = true;
-    int pass = 0, o = 0;
-    int ch_res = K_MEM, ch_cnt = 0, ch_st = 0, ch_ret = 0;
-    i64 ch_sum = 0;
-    double ch_N = 0;
-    int state = S_TASK, rq_res = K_MEM, rq_mode = 0;
-    LBase rq_b = {0, 0, 1};
-    double rq_N = 0;
-    bool pend = false; /* a consume step queued the next request itself */
-    #pragma unroll 1
-    for (;;) {
-        /* ---- advance until a fixed point is requested */
-        bool want = pend;
-        pend = false;
-        #pragma unroll 1
-        while (!want) {
-            switch (state) {
-            case S_TASK: {
-                if (k == n) return RTGPU_SCHEDULABLE;
-                if (k > 0) lat_view(tm, c, k - 1); /* counts of tasks before k are final */
-                const int inf = info[k];
-                m = li_m(inf);
-                p = li_p(inf);
-                gpu = li_gpu(inf);
-                D = c.D()[k];
-                B = c.B()[k];
-                sClu = c.sClu()[k];
-                glo = ghi = 0;
-                if (gpu) {
-                    const int gm = c.gmin()[k];
-                    rest_min -= gm;
-                    const i64 gmax = GN - used - rest_min;
-                    if (gmax < gm) return RTGPU_UNSCHEDULABLE;
-                    glo = gm;
-                    ghi = (int)gmax;
-                }
-                evals++;
-                mr_ub = 0;
-                sum_mr = -1;
-                bsum = 0;
-                sum_cr = -3;
-                rmax_exact = true;
-                if (p == 0) {
-                    sum_mr = 0;
-                    state = S_SEARCH;
-                    break;
-                }
-                /* the longest copy's response bounds every MR: first the
-                 * previous task's offset grown by half, verified as a
-                 * pre-fixed point (lfp <= f(b + N) <= D), then exactly */
-                const Seg32 ml_hi = c.segs(k) + 2 * m + p;
-                i64 bmax = 0;
-                #pragma unroll 1
-                for (int j = 0; j < p; j++) {
-                    bmax = tmax(bmax, (i64)ml_hi[j] + B);
-                    bsum += ml_hi[j] + B;
-                }
-                lbm = {bmax, 0, 1};
-                rq_res = K_MEM;
-                rq_b = lbm;
-                const double Ng = ceil(1.5 * mg) + 1.0;
-#ifndef RTGPU_LAT_NOGUESS
-                if (mg >= 1.0 && !lb_over(lbm, Ng, D)) {
-                    rq_N = Ng;
-                    rq_mode = 1;
-                    state = S_MEMG;
-                } else
-#endif
-                {
-                    (void)Ng;
-                    rq_N = (mw.bi >= 0 && lb_le(mw, lbm)) ? mwN : 0.0;
-                    rq_mode = 0;
-                    state = S_MEMX;
-                }
-                want = true;
-                break;
-            }
-            case S_SEARCH:
-                cand = gpu ? glo : 0;
-                lo = glo;
-                hi = ghi;
-                sphase = gpu ? 0 : 3;
-                state = S_PASS;
-                break;
-            case S_PASS:
-                gr = lat_grup(c, k, cand);
-                pass = 0;
-                state = S_R2;
-                break;
-            case S_R2: {
-                /* R2 (analysis.py:214): pass 0 with the bound on sum MR (a
-                 * pass is then exact), pass 1 with the exact sum */
-                const i64 smr = pass == 0 ? (p > 0 ? mr_ub : 0) : sum_mr;
-                b2 = {gr.bi + smr + sClu, gr.bf, gr.d};
-                const double nd = (double)(D - b2.bi - (b2.bf > 0 ? 1 : 0));
-                rq_res = K_CPU;
-                rq_b = b2;
-#ifndef RTGPU_LAT_NODCHECK
-                if (nd >= 0) {
-                    rq_N = nd;
-                    rq_mode = 1;
-                    state = S_R2CHK;
-                } else
-#endif
-                {
-                    (void)nd;
-                    rq_N = (cw.bi >= 0 && lb_le(cw, b2)) ? cwN : 0.0;
-                    rq_mode = 0;
-                    state = S_R2LFP;
-                }
-                want = true;
-                break;
-            }
-            case S_NEXTR2:
-                if (pass == 1 || p == 0) {
-                    state = S_R1;
-                    break;
-                }
-                pass = 1;
-                if (!rmax_exact) { /* the verified guess was too loose for R2 */
-                    rq_res = K_MEM;
-                    rq_b = lbm;
-                    rq_N = 0.0;
-                    rq_mode = 0;
-                    state = S_RMAX2;
-                    want = true;
-                    break;
-                }
-                if (sum_mr < 0) { /* the exact memory responses, every copy */
-                    const Seg32 ml_hi = c.segs(k) + 2 * m + p;
-                    tm.pfor(p, [&](int j) { c.bases()[j] = ml_hi[j] + B; });
-                    ch_res = K_MEM;
-                    ch_cnt = p;
-                    ch_ret = 0;
-                    state = S_CHAIN;
-                    ch_st = -1;
-                    break;
-                }
-                if (sum_mr == mr_ub) {
-                    state = S_R1;
-                    break;
-                }
-                state = S_R2;
-                break;
-            case S_R1:
-                if (sum_cr == -3) { /* the CPU segment responses (no dependence on g) */
-                    const Seg32 cl_hi = c.segs(k) + m;
-                    tm.pfor(m, [&](int j) { c.bases()[j] = cl_hi[j]; });
-                    ch_res = K_CPU;
-                    ch_cnt = m;
-                    ch_ret = 1;
-                    state = S_CHAIN;
-                    ch_st = -1;
-                    break;
-                }
-                /* R1 = GR up + sum MR + sum CR (analysis.py:207) */
-                o = sum_cr < 0 ? 0 : (lb_over(LBase{gr.bi + sum_mr + sum_cr, gr.bf, gr.d}, 0.0, D) ? 0 : 1);
-                state = S_RESULT;
-                break;
-            case S_CHAIN: {
-                if (ch_st < 0) {
-                    /* ascending bases (lfp(b') - b' >= lfp(b) - b): ranks */
-                    i64 *bs = c.bases();
-                    int *ord = c.ord();
-                    const int cnt = ch_cnt;
-                    tm.pfor(cnt, [&](int j) {
-                        int rk = 0;
-                        #pragma unroll 1
-                        for (int x = 0; x < cnt; x++) rk += (bs[x] < bs[j] || (bs[x] == bs[j] && x < j)) ? 1 : 0;
-                        ord[rk] = j;
-                    });
-                    ch_st = 0;
-                    ch_sum = 0;
-                    ch_N = 0;
-                }
-                if (ch_st == ch_cnt) { /* the chain's sum */
-                    tm.sync();
-                    if (ch_ret == 0) {
-                        sum_mr = ch_sum;
-                        state = sum_mr == mr_ub ? S_R1 : S_R2;
-                    } else {
-                        sum_cr = ch_sum;
-                        state = S_R1;
-                    }
-                    break;
-                }
-                rq_res = ch_res;
-                rq_b = {c.bases()[c.ord()[ch_st]], 0, 1};
-                rq_N = ch_N;
-                rq_mode = 0;
-                state = S_CHAINR;
-                want = true;
-                break;
-            }
-            case S_RESULT:
-                /* smallest passing count: glo, else ghi, else bisection */
-                if (o < 0) return ST_ESCALATE;
-                if (sphase == 3) {
-                    if (!o) return RTGPU_UNSCHEDULABLE;
-                    k++;
-                    state = S_TASK;
-                    break;
-                }
-                if (sphase == 0) {
-                    if (o) {
-                        cand = glo;
-                        sphase = 9; /* done */
-                    } else if (glo >= ghi) {
-                        return RTGPU_UNSCHEDULABLE;
-                    } else {
-                        sphase = 1;
-                        cand = ghi;
-                        state = S_PASS;
-                        break;
-                    }
-                } else {
-                    if (sphase == 1) {
-                        if (!o) return RTGPU_UNSCHEDULABLE;
-                        sphase = 2;
-                    } else if (o) {
-                        hi = cand;
-                    } else {
-                        lo = cand;
-                    }
-                    if (hi - lo <= 1) {
-                        cand = hi;
-                        sphase = 9;
-                    } else {
-                        cand = lo + (hi - lo) / 2;
-                        state = S_PASS;
-                        break;
-                    }
-                }
-                /* the count of task k is final */
-                if (tm.leader()) c.g()[k] = cand;
-                tm.sync();
-                used += cand;
-                k++;
-                state = S_TASK;
-                break;
-            default:
-                return ST_ESCALATE;
-            }
-        }
-        /* ---- the one fixed-point call */
-#ifdef RTGPU_LAT_INLINE
-        const double r = lfp_lat_body(tm, lat_key(c, k, rq_res), rq_b, rq_N, D, rq_mode);
-#else
-        const double r = lfp_lat(tm, lat_key(c, k, rq_res), rq_b, rq_N, D, rq_mode);
-#endif
-        /* ---- consume */
-        switch (state) {
-        case S_MEMG:
-            if (r >= 0) { /* verified: rmax <= r */
-                rmax_exact = false;
-                mg = r;
-                mr_ub = (i64)p * (i64)r + bsum;
-                state = S_SEARCH;
-            } else { /* the exact fixed point next */
-                rq_N = (mw.bi >= 0 && lb_le(mw, lbm)) ? mwN : 0.0;
-                rq_mode = 0;
-                state = S_MEMX;
-                pend = true;
-            }
-            break;
-        case S_MEMX:
-            if (r == -2.0) return ST_ESCALATE;
-            if (r < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None at every count */
-            mw = lbm;
-            mwN = r;
-            mg = r;
-            mr_ub = (i64)p * (i64)r + bsum;
-            state = S_SEARCH;
-            break;
-        case S_R2CHK:
-            if (r >= 0) {
-                o = 1;
-                state = S_RESULT;
-            } else { /* the fixed point itself next */
-                rq_N = (cw.bi >= 0 && lb_le(cw, b2)) ? cwN : 0.0;
-                rq_mode = 0;
-                state = S_R2LFP;
-                pend = true;
-            }
-            break;
-        case S_R2LFP:
-            if (r == -2.0) {
-                o = -1;
-                state = S_RESULT;
-            } else if (r >= 0) {
-                cw = b2;
-                cwN = r;
-                o = 1;
-                state = S_RESULT;
-            } else {
-                state = S_NEXTR2;
-            }
-            break;
-        case S_RMAX2: {
-            if (r < 0) { /* cannot be None below a verified bound */
-                o = -1;
-                state = S_RESULT;
-                break;
-            }
-            rmax_exact = true;
-            mw = lbm;
-            mwN = r;
-            mg = r;
-            const i64 ub = (i64)p * (i64)r + bsum;
-            if (ub < mr_ub) { /* R2 again with the exact bound */
-                mr_ub = ub;
-                pass = 0;
-                state = S_R2;
-            } else {
-                pass = 0;
-                state = S_NEXTR2;
-            }
-            break;
-        }
-        case S_CHAINR:
-            if (r < 0) {
-                tm.sync();
-                if (r == -2.0) {
-                    o = -1;
-                    state = S_RESULT;
-                } else if (ch_ret == 0) {
-                    o = -1; /* an MR None below the longest copy's bound: cannot be */
-                    state = S_RESULT;
-                } else {
-                    sum_cr = -1;
-                    state = S_R1;
-                }
-                break;
-            }
-            ch_sum += rq_b.bi + (i64)r;
-            ch_N = r;
-            ch_st++;
-            state = S_CHAIN;
-            break;
-        default:
-            return ST_ESCALATE;
-        }
-    }
-}
-
 /* The whole RTGPU analysis of one compact blob: status, allocation (vsm),
  * the number of task evaluations, and with `bounds` the report's end-to-end
  * bounds (e2e / den, else unused). */
@@ -1362,10 +978,6 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
     });
     tm.pfor(n, [&](int k) { c.B()[k] = *(const i64 *)(c.VC() + (size_t)k * c.L.SC); });
     (void)bases;
-#ifndef RTGPU_LAT_LOOPS
-    int st = lat_search(tm, c, need, evals);
-    if (st == ST_ESCALATE) return ST_ESCALATE;
-#else
     i64 used = 0, rest_min = need;
     /* warm starts: the last converged memory / CPU fixed point (base, N);
      * valid for any later task (hp(k) only grows) at a base >= its base */
@@ -1557,7 +1169,6 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         tm.sync();
         used += g;
     }
-#endif
     if (st == RTGPU_SCHEDULABLE) tm.pfor(n, [&](int i) { vsm[i] = li_gpu(c.info()[i]) ? 2 * c.g()[i] : 0; });
     if (!bounds) return st;
     int have = n - 1;
