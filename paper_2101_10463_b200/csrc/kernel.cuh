@@ -18,6 +18,10 @@
 
 namespace rtgpu {
 
+#ifndef RTGPU_MAX_CHUNKS
+#define RTGPU_MAX_CHUNKS 32
+#endif
+
 struct KParams {
     const i64 *blobs, *set_off, *task_base;
     i64 n_sets;
@@ -39,9 +43,11 @@ struct KParams {
     int last_stage = 3;        /* escalating past this general stage is RTGPU_RANGE (3; 2 in
                                 * verdict runs, whose general stages are int64 then int128) */
     /* streamed input (end-to-end path): set s of chunk c = the c with
-     * n*c/chunks <= s < n*(c+1)/chunks is readable once chunk_flag[c] ==
-     * epoch (the copy stream writes it after the chunk's H2D copy) */
+     * chunk_begin[c] <= s < chunk_begin[c + 1] is readable once
+     * chunk_flag[c] == epoch (the copy stream writes it after the chunk's
+     * H2D copy) */
     const unsigned long long *chunk_flag = nullptr;
+    i64 chunk_begin[RTGPU_MAX_CHUNKS + 1];
     /* set to epoch by the first warp whose wait times out: every other warp
      * then stops waiting at once and the host re-runs the batch unstreamed */
     unsigned long long *chunk_abort = nullptr;
@@ -239,11 +245,11 @@ __device__ __forceinline__ bool wait_chunk(const KParams &p, i64 s, int lane) {
      * GPU -- after ~2^23 polls (seconds) the set is reported undecided */
     int ok = 1;
     if (lane == 0) {
-        const i64 n = p.n_sets, C = p.chunks;
-        i64 c = s * C / n;
-        while (c + 1 < C && n * (c + 1) / C <= s) c++;
-        while (c > 0 && n * c / C > s) c--;
-        const bool first = s == n * c / C;
+        int c = 0;
+        #pragma unroll 1
+        for (int st = 16; st > 0; st >>= 1) /* last chunk with chunk_begin[c] <= s */
+            if (c + st < p.chunks && p.chunk_begin[c + st] <= s) c += st;
+        const bool first = s == p.chunk_begin[c];
         const unsigned long long *f = p.chunk_flag + c;
         unsigned long long v;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");

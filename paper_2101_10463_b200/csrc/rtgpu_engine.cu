@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 
 #include "../../include/rtgpu.h"
@@ -58,7 +59,7 @@ struct DevBuf {
 };
 
 DevBuf g_scratch; /* counters + escalation lists */
-const int MAX_CHUNKS = 32;
+const int MAX_CHUNKS = RTGPU_MAX_CHUNKS;
 /* [0..7] stage counters, [8, 8 + MAX_CHUNKS) per-chunk work counters,
  * [8 + MAX_CHUNKS, 8 + 2 MAX_CHUNKS) chunk arrival flags (streamed path) */
 /* [8+2*MAX_CHUNKS]: stream abort word, [9+2*MAX_CHUNKS]: lattice list stage's work counter */
@@ -429,6 +430,28 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
          * warps wait (acquire loads) only for chunks not yet there.  No
          * per-chunk launches, no per-chunk tails. */
         const int chunks = (int)std::min<i64>(MAX_CHUNKS, std::max<i64>(1, n_sets / 2048));
+        /* chunk sizes: a half-size first chunk (the kernel starts sooner),
+         * equal chunks, then six halving ones -- after the last copy lands
+         * the kernel still has that chunk's sets to analyse, and a set's
+         * latency is what the call waits for (e2e trace: 0.41 ms with equal
+         * chunks) */
+        i64 cb[MAX_CHUNKS + 1];
+        {
+            double w[MAX_CHUNKS], tot = 0;
+            const int tail = chunks >= 16 ? 6 : 0;
+            for (int c = 0; c < chunks; c++) {
+                w[c] = c == 0 && chunks > 1 ? 0.5 : 1.0;
+                if (c >= chunks - tail) w[c] = std::ldexp(1.0, -(c - (chunks - tail) + 1));
+                tot += w[c];
+            }
+            double acc = 0;
+            cb[0] = 0;
+            for (int c = 0; c < chunks; c++) {
+                acc += w[c];
+                cb[c + 1] = c + 1 == chunks ? n_sets : std::min<i64>(n_sets, (i64)(acc / tot * (double)n_sets));
+                if (cb[c + 1] < cb[c]) cb[c + 1] = cb[c];
+            }
+        }
         static unsigned long long *h_epoch = nullptr;
         static unsigned long long epoch = 0;
         if (!h_epoch && cudaMallocHost(&h_epoch, 8) != cudaSuccess) {
@@ -449,7 +472,7 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         cudaMemcpyAsync(g_h_off.p, set_off, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
         cudaMemcpyAsync(g_h_tb.p, task_base, (n_sets + 1) * 8, cudaMemcpyHostToDevice, cp);
         auto enqueue_chunk = [&](int c) {
-            const i64 a = n_sets * c / chunks, b = n_sets * (c + 1) / chunks;
+            const i64 a = cb[c], b = cb[c + 1];
             const size_t w0 = (size_t)set_off[a], w1 = (size_t)set_off[b];
             cudaMemcpyAsync((i64 *)g_h_blobs.p + w0, blobs + w0, (w1 - w0) * 8, cudaMemcpyHostToDevice, cp);
             /* the arrival flag: a stream memory operation when the driver
@@ -466,18 +489,35 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         q.chunk_abort = p.ctr + 8 + 2 * MAX_CHUNKS;
         q.epoch = epoch;
         q.chunks = chunks;
+        for (int c = 0; c <= chunks; c++) q.chunk_begin[c] = cb[c];
         /* the first chunk, then the kernel, then the rest: the kernel starts
          * as soon as chunk 0 lands instead of after the host has enqueued
          * every copy */
+        /* RTGPU_E2E_TRACE=1: the stream timeline of the call on stderr */
+        static const bool trace = [] {
+            const char *v = getenv("RTGPU_E2E_TRACE");
+            return v && v[0] == '1';
+        }();
+        static cudaEvent_t tev[6];
+        static bool tev_init = false;
+        if (trace && !tev_init) {
+            for (auto &e : tev) cudaEventCreate(&e);
+            tev_init = true;
+        }
+        if (trace) cudaEventRecord(tev[0], cs);
         enqueue_chunk(0);
+        if (trace) cudaEventRecord(tev[1], cp);
         int rc = launch_front_f64(q, cs);
+        if (trace) cudaEventRecord(tev[2], cs);
         for (int c = 1; c < chunks; c++) enqueue_chunk(c);
+        if (trace) cudaEventRecord(tev[3], cp);
         if (!rc) {
             /* every chunk has arrived once the fast kernel is done */
             cudaEventRecord(g_ev_chunk[0], cp);
             cudaStreamWaitEvent(cs, g_ev_chunk[0], 0);
             rc = launch_general(p, cs);
         }
+        if (trace) cudaEventRecord(tev[4], cs);
         if (rc) return rc;
         /* sets beyond the sampled layout (mixed batches): rare; the host
          * learns their count, scans the true dims and runs them through the
@@ -519,10 +559,17 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
             cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, cs);
             cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, cs);
             cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, cs);
+            if (trace) cudaEventRecord(tev[5], cs);
             e = cudaStreamSynchronize(cs);
             if (e != cudaSuccess) {
                 set_err("rtgpu_analyze_host", e);
                 return -8;
+            }
+            if (trace) {
+                float t[6] = {0};
+                for (int i = 1; i < 6; i++) cudaEventElapsedTime(&t[i], tev[0], tev[i]);
+                fprintf(stderr, "e2e trace ms: chunk0 copied %.3f | kernel done %.3f | all copies %.3f | "
+                        "general done %.3f | results back %.3f\n", t[1], t[2], t[3], t[4], t[5]);
             }
             return 0;
         }
