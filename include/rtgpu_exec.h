@@ -61,6 +61,11 @@ typedef struct {
                                    * response as the job sees it)            */
     double seg_worst_mhz[15];     /* SM clock during the worst-span launch     */
     double min_mhz;               /* lowest SM clock seen in any launch        */
+    int32_t seg_worst_smsp[15];   /* worst-span launch: most participating warps
+                                   * on one SM sub-partition (%warpid % 4) of
+                                   * any of its SMs (2 = even, two 4-warp
+                                   * blocks per SM)                           */
+    int32_t smsp_max;             /* the same over every launch                */
 } rtgpu_exec_result;
 
 /* Host-side resource models of rtgpu_exec_run (rtgpu_exec_configure):

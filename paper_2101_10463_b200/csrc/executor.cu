@@ -58,6 +58,8 @@ struct Ctl {
     unsigned bitems[16];          /* items of the first 16 participating blocks */
     unsigned long long cyc0, ns0; /* block 0 of the participants: SM clock and */
     unsigned long long cyc1, ns1; /* global time at its start and end           */
+    unsigned smsp[256];           /* per SM: participating warps per SM sub-
+                                   * partition (%warpid % 4), 8 bits each       */
 };
 
 struct SegArgs {
@@ -132,6 +134,11 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
      * current one is computed and only consumed after it, so the atomic's
      * round trip never sits on the critical path. */
     const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        unsigned wid;
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+        gadd32(&a.ctl->smsp[sm & 255], 1u << (8 * (wid & 3)));
+    }
     const long long witems = a.items * (long long)(blockDim.x >> 5);
     float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f;
     /* two claims in flight: a claim is consumed two items after it was
@@ -318,6 +325,7 @@ struct LaunchDetail {
     double skew_us;     /* first -> last participating block start             */
     int items_min, items_max;
     double mhz;         /* SM clock over the first participant's run            */
+    int smsp_max;       /* most participating warps on one SM sub-partition     */
 };
 
 void decode_ctl(const Ctl &c, unsigned *nb, double *span_us, LaunchDetail *d);
@@ -342,6 +350,9 @@ void decode_ctl(const Ctl &c, unsigned *nb, double *span_us, LaunchDetail *d) {
             d->items_min = std::min(d->items_min, (int)c.bitems[b]);
             d->items_max = std::max(d->items_max, (int)c.bitems[b]);
         }
+        d->smsp_max = 0;
+        for (int sm = 0; sm < 256; sm++)
+            for (int k = 0; k < 4; k++) d->smsp_max = std::max(d->smsp_max, (int)((c.smsp[sm] >> (8 * k)) & 255));
     }
 }
 
@@ -802,7 +813,9 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
                         R.seg_worst_items[s][0] = det.items_min;
                         R.seg_worst_items[s][1] = det.items_max;
                         R.seg_worst_mhz[s] = det.mhz;
+                        R.seg_worst_smsp[s] = det.smsp_max;
                     }
+                    R.smsp_max = std::max(R.smsp_max, det.smsp_max);
                     if (det.mhz > 0 && (R.min_mhz == 0 || det.mhz < R.min_mhz)) R.min_mhz = det.mhz;
                     float kms = 0;
                     cudaEventElapsedTime(&kms, L.k0[s], L.k1[s]);

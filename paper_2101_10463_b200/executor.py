@@ -51,7 +51,8 @@ class ExecResultC(ctypes.Structure):
                 ("seg_worst_skew_us", ctypes.c_double * 15),
                 ("seg_worst_items", (ctypes.c_int32 * 2) * 15),
                 ("seg_max_wall_us", ctypes.c_double * 15),
-                ("seg_worst_mhz", ctypes.c_double * 15), ("min_mhz", ctypes.c_double)]
+                ("seg_worst_mhz", ctypes.c_double * 15), ("min_mhz", ctypes.c_double),
+                ("seg_worst_smsp", ctypes.c_int32 * 15), ("smsp_max", ctypes.c_int32)]
 
 CPU_PARALLEL, CPU_FP_ONE_CORE = 0, 1   # include/rtgpu_exec.h host resource models
 BUS_FREE, BUS_FP = 0, 1
@@ -422,8 +423,10 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
                           "worst_launch": [{"skew_us": round(r.seg_worst_skew_us[j], 1),
                                             "sm_mhz": round(r.seg_worst_mhz[j]),
                                             "items": [int(r.seg_worst_items[j][0]),
-                                                      int(r.seg_worst_items[j][1])]}
+                                                      int(r.seg_worst_items[j][1])],
+                                            "smsp_max_warps": int(r.seg_worst_smsp[j])}
                                            for j in range(len(grs))],
+                          "smsp_max_warps": int(r.smsp_max),
                           "min_sm_mhz": round(r.min_mhz),
                           "max_copy_us": round(r.max_copy_us, 1),
                           "max_bus_wait_us": round(r.max_bus_wait_us, 1),

@@ -70,6 +70,31 @@ class PackedBatch:
         return len(self.metas)
 
 
+class _NativeMetas:
+    """SetMeta records of a natively packed batch, built when read: a sweep
+    that wants verdicts only never pays for them."""
+
+    __slots__ = ("tasksets", "scales", "orders", "set_off", "task_base")
+
+    def __init__(self, tasksets, scales, orders, set_off, task_base):
+        self.tasksets, self.scales, self.orders = tasksets, scales, orders
+        self.set_off, self.task_base = set_off, task_base
+
+    def __len__(self) -> int:
+        return len(self.scales)
+
+    def __getitem__(self, k: int) -> SetMeta:
+        if k < 0:
+            k += len(self.scales)
+        if not 0 <= k < len(self.scales):
+            raise IndexError(k)
+        return SetMeta(self.tasksets[k], self.orders[k], self.scales[k], int(self.set_off[k]),
+                       int(self.task_base[k]))
+
+    def __iter__(self):
+        return (self[k] for k in range(len(self.scales)))
+
+
 def _lcm_all(values) -> int:
     out = 1
     for v in values:
@@ -208,10 +233,8 @@ def pack_tasksets(tasksets: Sequence[TaskSet]) -> PackedBatch:
             blobs = np.frombuffer(b, dtype=np.int64)
             set_off = np.frombuffer(so, dtype=np.int64)
             task_base = np.frombuffer(tb, dtype=np.int64)
-            metas = [SetMeta(ts, tuple(ts.tasks[i] for i in order), int(S), int(set_off[k]),
-                             int(task_base[k]))
-                     for k, (ts, S, order) in enumerate(zip(tasksets, scales, orders))]
-            return PackedBatch(blobs, set_off, task_base, metas)
+            return PackedBatch(blobs, set_off, task_base,
+                               _NativeMetas(tasksets, scales, orders, set_off, task_base))
     return pack_tasksets_py(tasksets)
 
 

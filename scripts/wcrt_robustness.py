@@ -17,10 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--wide", action="store_true")
 ap.add_argument("--seeds", type=int, default=8)
 ap.add_argument("--horizon-s", type=float, default=1.0)
+ap.add_argument("--seed-list", default="", help="comma-separated seeds (overrides --seeds)")
 args = ap.parse_args()
 levels = [(8, 16), (16, 28), (28, 40)] if args.wide else [2.5, 3.0, 4.0]
+seeds = [int(x) for x in args.seed_list.split(",") if x] or list(range(1, args.seeds + 1))
 out = []
-for seed in range(1, args.seeds + 1):
+for seed in seeds:
     for lv in levels:
         kw = dict(width=lv) if args.wide else dict(utilization=lv)
         r = ex.wcrt_experiment(n_tasks=4, m=3, horizon_us=args.horizon_s * 1e6, seed=seed, **kw)
@@ -32,7 +34,8 @@ for seed in range(1, args.seeds + 1):
                "jobs": [t["jobs"] for t in r.tasks], "note": r.note,
                "blocks_per_launch_vs_2g": [(t["blocks_per_launch"], 2 * t["sms"]) for t in r.tasks],
                "kernel_span_vs_gr_up": [t["kernel_span_us_vs_gr_up"] for t in r.tasks],
-               "worst_launch": [t["worst_launch"] for t in r.tasks]}
+               "worst_launch": [t["worst_launch"] for t in r.tasks],
+               "smsp_max_warps": max((t["smsp_max_warps"] for t in r.tasks), default=0)}
         out.append(rec)
         print(json.dumps(rec), flush=True)
 ok = [x for x in out if x["schedulable"]]
