@@ -115,6 +115,13 @@ int rtgpu_exec_kernel_ms_stress(const uint32_t *mask, int nslots, int64_t items,
  * launch and polled completion -- the executor's per-kernel overhead. */
 int rtgpu_exec_launch_us(const uint32_t *mask, int reps, float *us_out);
 
+/* The kernel launches of the last rtgpu_exec_run, 7 doubles each: task
+ * index, kernel segment, first participating block's start (us of
+ * %globaltimer), on-GPU span (us), fewest / most work items of a traced
+ * warp, SM clock (MHz).  Writes min(count, max_records) records and returns
+ * the count. */
+int rtgpu_exec_launch_log(double *out, int max_records);
+
 /* Host wall time (ms) of `reps` pinned-host copies of `bytes` (to_device:
  * H2D, else D2H): enqueue and polled completion, as the run loop does. */
 int rtgpu_exec_copy_ms(int64_t bytes, int to_device, int reps, float *ms_out);

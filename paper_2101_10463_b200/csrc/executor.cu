@@ -179,6 +179,19 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
 
 char g_err[256] = "";
 
+/* every kernel launch of the last rtgpu_exec_run: task, segment, first
+ * participating block's start (%globaltimer ns), span (us), fewest / most
+ * items of a traced warp, SM clock -- read by rtgpu_exec_launch_log */
+struct LaunchRec {
+    int task, seg;
+    unsigned long long t0_ns;
+    double span_us;
+    int items_min, items_max;
+    double mhz;
+};
+std::mutex g_log_mu;
+std::vector<LaunchRec> g_log;
+
 constexpr int RING = 16; /* control blocks / event pairs per lane: one per kernel of a job */
 
 struct Lane {
@@ -676,6 +689,23 @@ int rtgpu_exec_probe(const uint32_t *mask, int nslots, int64_t items, int iters,
     return 0;
 }
 
+int rtgpu_exec_launch_log(double *out, int max_records) {
+    std::lock_guard<std::mutex> g(g_log_mu);
+    const int n = (int)std::min<size_t>(g_log.size(), (size_t)std::max(0, max_records));
+    for (int k = 0; k < n; k++) {
+        const LaunchRec &r = g_log[k];
+        double *o = out + 7 * (size_t)k;
+        o[0] = r.task;
+        o[1] = r.seg;
+        o[2] = (double)r.t0_ns * 1e-3;
+        o[3] = r.span_us;
+        o[4] = r.items_min;
+        o[5] = r.items_max;
+        o[6] = r.mhz;
+    }
+    return (int)g_log.size();
+}
+
 int rtgpu_exec_configure(int cpu_mode, int bus_mode) {
     if (cpu_mode < 0 || cpu_mode > 1 || bus_mode < 0 || bus_mode > 1) {
         strcpy(g_err, "rtgpu_exec_configure: unknown mode");
@@ -700,6 +730,10 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
     if (n_tasks < 1 || n_tasks > 64) {
         strcpy(g_err, "1..64 tasks");
         return -1;
+    }
+    {
+        std::lock_guard<std::mutex> g(g_log_mu);
+        g_log.clear();
     }
     std::vector<Lane> lanes(n_tasks);
     for (int i = 0; i < n_tasks; i++) {
@@ -808,6 +842,12 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
                     double span = 0;
                     LaunchDetail det;
                     decode_ctl(L.hring[s], &nb, &span, &det);
+                    {
+                        std::lock_guard<std::mutex> g(g_log_mu);
+                        if (g_log.size() < (1u << 20))
+                            g_log.push_back({i, s, ~L.hring[s].inv_start, span, det.items_min, det.items_max,
+                                             det.mhz});
+                    }
                     if (span > R.seg_max_span_us[s]) {
                         R.seg_worst_skew_us[s] = det.skew_us;
                         R.seg_worst_items[s][0] = det.items_min;

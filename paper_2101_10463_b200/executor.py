@@ -195,6 +195,11 @@ class WcrtReport:
     bus_mode: int = BUS_FP
     calibration: list = field(default_factory=list)  # per kernel: items, t1, t2, alpha
     note: str = ""
+    # launches over their Lemma-4 bound, each with the other tasks' launches
+    # that overlapped it in GPU time (span / GR_up of each) -- is a slowdown
+    # one partition's, or GPU-wide?
+    overruns: list = field(default_factory=list)
+    launch_ratio_pcts: dict = field(default_factory=dict)  # span / GR_up percentiles over all launches
 
 
 def _ceil_margin(x_us: float, margin: float) -> int:
@@ -238,6 +243,34 @@ def calibrate_kernel(items: int, iters: int, reps: int = 4, margin: float = MARG
     alpha = Fraction(max(100, pct), 100)
     return KernelCal(items, iters, t1u, t2u, alpha, int(min(t1) * 1e3 * 0.95),
                      _ceil_margin(t1u, margin))
+
+
+def launch_log():
+    """The last run's kernel launches (rtgpu_exec_launch_log): dicts with task,
+    seg, t0_us (%globaltimer), span_us, items (min, max of traced warps), mhz."""
+    L = _lib()
+    L.rtgpu_exec_launch_log.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+    n = L.rtgpu_exec_launch_log(None, 0)
+    buf = (ctypes.c_double * (7 * max(n, 1)))()
+    n = L.rtgpu_exec_launch_log(buf, n)
+    return [{"task": int(buf[7 * k]), "seg": int(buf[7 * k + 1]), "t0_us": buf[7 * k + 2],
+             "span_us": buf[7 * k + 3], "items": (int(buf[7 * k + 4]), int(buf[7 * k + 5])),
+             "mhz": buf[7 * k + 6]} for k in range(n)]
+
+
+def _overrun_context(log, grs_of, limit: int = 12):
+    """Launches over their bound and what ran beside them."""
+    ratio = lambda e: e["span_us"] / grs_of[e["task"]][e["seg"]]  # noqa: E731
+    out = []
+    for e in sorted((e for e in log if ratio(e) > 1.0), key=ratio, reverse=True)[:limit]:
+        a0, a1 = e["t0_us"], e["t0_us"] + e["span_us"]
+        beside = [{"task": o["task"], "seg": o["seg"], "ratio": round(ratio(o), 3),
+                   "overlap_us": round(min(a1, o["t0_us"] + o["span_us"]) - max(a0, o["t0_us"]), 1)}
+                  for o in log if o is not e and o["t0_us"] < a1 and o["t0_us"] + o["span_us"] > a0]
+        out.append({"task": e["task"], "seg": e["seg"], "ratio": round(ratio(e), 3),
+                    "span_us": round(e["span_us"], 1), "t0_ms": round((a0 - log[0]["t0_us"]) * 1e-3, 3),
+                    "items": e["items"], "mhz": round(e["mhz"]), "beside": beside})
+    return out
 
 
 def run_tasks(defs, partitions, iters: int, horizon_us: float, two_copy: bool = True,
@@ -433,6 +466,15 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
                           "blocks_per_launch": [int(r.min_blocks), int(r.max_blocks)],
                           "gr_up_us": float(max(grs)), "deadline_us": d.deadline_us,
                           "deadline_misses": int(r.deadline_misses)})
+    grs_of = [[float(gpu_response_bounds(g, 2 * len(sms)).hi) for g in s.gpu_segments]
+              for s, sms in zip(specs, parts)]
+    log = launch_log()
+    if log:
+        out.overruns = _overrun_context(log, grs_of)
+        rs = np.array([e["span_us"] / grs_of[e["task"]][e["seg"]] for e in log])
+        out.launch_ratio_pcts = {"launches": len(rs), "p50": round(float(np.percentile(rs, 50)), 3),
+                                 "p99": round(float(np.percentile(rs, 99)), 3),
+                                 "max": round(float(rs.max()), 3), "over_1": int((rs > 1).sum())}
     out.max_ratio = max(ratios)
     out.all_within_bound = all(x <= 1.0 for x in ratios)
     out.kernels_within_bound = kok

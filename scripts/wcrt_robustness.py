@@ -35,7 +35,8 @@ for seed in seeds:
                "blocks_per_launch_vs_2g": [(t["blocks_per_launch"], 2 * t["sms"]) for t in r.tasks],
                "kernel_span_vs_gr_up": [t["kernel_span_us_vs_gr_up"] for t in r.tasks],
                "worst_launch": [t["worst_launch"] for t in r.tasks],
-               "smsp_max_warps": max((t["smsp_max_warps"] for t in r.tasks), default=0)}
+               "smsp_max_warps": max((t["smsp_max_warps"] for t in r.tasks), default=0),
+               "launch_ratio_pcts": r.launch_ratio_pcts, "overruns": r.overruns}
         out.append(rec)
         print(json.dumps(rec), flush=True)
 ok = [x for x in out if x["schedulable"]]
