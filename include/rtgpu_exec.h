@@ -122,6 +122,13 @@ int rtgpu_exec_launch_us(const uint32_t *mask, int reps, float *us_out);
  * the count. */
 int rtgpu_exec_launch_log(double *out, int max_records);
 
+/* The last rtgpu_exec_run's stall sentinel: one thread on an SM no task used
+ * read %globaltimer every ~2 us for the whole run; each record (2 doubles,
+ * us of %globaltimer, the launch log's time base) is an interval over 50 us
+ * in which it did not run.  *sentinel_sm = that SM, -1 if every SM was in a
+ * partition (no sentinel).  Returns the count. */
+int rtgpu_exec_stall_log(double *out, int max_records, int *sentinel_sm);
+
 /* Host wall time (ms) of `reps` pinned-host copies of `bytes` (to_device:
  * H2D, else D2H): enqueue and polled completion, as the run loop does. */
 int rtgpu_exec_copy_ms(int64_t bytes, int to_device, int reps, float *ms_out);

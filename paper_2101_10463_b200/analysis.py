@@ -25,7 +25,9 @@ def analyze_batch(tasksets: Sequence[TaskSet], method: AnalysisMethod = Analysis
     method = AnalysisMethod(method)
     if not tasksets:
         return []
-    batch = pack_tasksets(tasksets)
+    # compact blobs (int32 segment areas: the fast / lattice kernels' form)
+    # unless the per-segment report needs the int64 detail layout
+    batch = pack_tasksets(tasksets, compact=not detail)
     flags = F_DETAIL if detail else F_BOUNDS
     res = engine.analyze_packed(batch.blobs, batch.set_off, batch.task_base,
                                 METHOD_CODES[method], flags, budget)

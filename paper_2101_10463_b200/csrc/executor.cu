@@ -177,6 +177,31 @@ __global__ void __launch_bounds__(128) persistent_segment(SegArgs a) {
     if (x0 + x1 + x2 == 12345.f) a.sink[blockIdx.x] = x0;
 }
 
+/* Stall sentinel: one thread on an SM no partition uses reads %globaltimer
+ * every ~2 us for the whole run and logs every gap above `thresh_ns` -- the
+ * intervals in which that SM (with the rest of the GPU, if the pause is
+ * GPU-wide) did not execute.  Every other block exits at once. */
+struct StallGap {
+    unsigned long long a, b;
+};
+
+__global__ void stall_sentinel(unsigned target_sm, const volatile int *stop, int *claim, StallGap *gaps,
+                               unsigned *ngaps, unsigned cap, unsigned long long thresh_ns) {
+    if (smid() != target_sm || threadIdx.x != 0) return;
+    if (atomicCAS(claim, 0, 1) != 0) return;
+    unsigned long long prev = gtimer();
+    for (unsigned it = 0;; it++) {
+        if ((it & 63) == 0 && *stop) break;
+        __nanosleep(2000);
+        const unsigned long long now = gtimer();
+        if (now - prev > thresh_ns) {
+            const unsigned k = atomicAdd(ngaps, 1u);
+            if (k < cap) gaps[k] = StallGap{prev, now};
+        }
+        prev = now;
+    }
+}
+
 char g_err[256] = "";
 
 /* every kernel launch of the last rtgpu_exec_run: task, segment, first
@@ -191,6 +216,8 @@ struct LaunchRec {
 };
 std::mutex g_log_mu;
 std::vector<LaunchRec> g_log;
+std::vector<StallGap> g_stalls; /* the last run's sentinel gaps */
+int g_sentinel_sm = -1;         /* the SM it ran on, -1 = none free */
 
 constexpr int RING = 16; /* control blocks / event pairs per lane: one per kernel of a job */
 
@@ -706,6 +733,17 @@ int rtgpu_exec_launch_log(double *out, int max_records) {
     return (int)g_log.size();
 }
 
+int rtgpu_exec_stall_log(double *out, int max_records, int *sentinel_sm) {
+    std::lock_guard<std::mutex> g(g_log_mu);
+    if (sentinel_sm) *sentinel_sm = g_sentinel_sm;
+    const int n = (int)std::min<size_t>(g_stalls.size(), (size_t)std::max(0, max_records));
+    for (int k = 0; k < n; k++) {
+        out[2 * k] = (double)g_stalls[k].a * 1e-3;
+        out[2 * k + 1] = (double)g_stalls[k].b * 1e-3;
+    }
+    return (int)g_stalls.size();
+}
+
 int rtgpu_exec_configure(int cpu_mode, int bus_mode) {
     if (cpu_mode < 0 || cpu_mode > 1 || bus_mode < 0 || bus_mode > 1) {
         strcpy(g_err, "rtgpu_exec_configure: unknown mode");
@@ -758,6 +796,26 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
     CoreFence fence;
     if (cpu_mode == RTGPU_EXEC_CPU_PARALLEL && (int)cpus.size() > n_tasks)
         fence.apply(std::vector<int>(cpus.begin(), cpus.begin() + n_tasks), cpus);
+    /* the stall sentinel on the first SM no task uses */
+    const int nsm = sm_count();
+    int free_sm = -1;
+    for (int sm = 0; sm < nsm && free_sm < 0; sm++) {
+        bool used = false;
+        for (int i = 0; i < n_tasks; i++) used = used || ((tasks[i].sm_mask[sm >> 5] >> (sm & 31)) & 1u);
+        if (!used) free_sm = sm;
+    }
+    const unsigned STALL_CAP = 4096;
+    cudaStream_t sst = nullptr;
+    char *sbuf = nullptr; /* stop flag, claim, count, gaps */
+    if (free_sm >= 0 && cudaStreamCreateWithFlags(&sst, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaMalloc(&sbuf, 64 + STALL_CAP * sizeof(StallGap)) == cudaSuccess) {
+        cudaMemsetAsync(sbuf, 0, 64, sst);
+        stall_sentinel<<<2 * nsm, 32, 0, sst>>>((unsigned)free_sm, (const volatile int *)sbuf, (int *)(sbuf + 4),
+                                                (StallGap *)(sbuf + 64), (unsigned *)(sbuf + 8), STALL_CAP,
+                                                50000ull);
+    } else {
+        free_sm = -1;
+    }
     auto t_start = clk::now() + std::chrono::milliseconds(50);
     std::vector<std::thread> th;
     for (int i = 0; i < n_tasks; i++) {
@@ -873,6 +931,23 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
     }
     for (auto &x : th) x.join();
     fence.restore();
+    {
+        std::lock_guard<std::mutex> g(g_log_mu);
+        g_stalls.clear();
+        g_sentinel_sm = free_sm;
+        if (free_sm >= 0) {
+            static const int one = 1;
+            cudaMemcpyAsync(sbuf, &one, sizeof one, cudaMemcpyHostToDevice, sst);
+            unsigned n = 0;
+            cudaMemcpyAsync(&n, sbuf + 8, sizeof n, cudaMemcpyDeviceToHost, sst);
+            cudaStreamSynchronize(sst);
+            n = std::min(n, STALL_CAP);
+            g_stalls.resize(n);
+            if (n) cudaMemcpy(g_stalls.data(), sbuf + 64, n * sizeof(StallGap), cudaMemcpyDeviceToHost);
+        }
+    }
+    if (sbuf) cudaFree(sbuf);
+    if (sst) cudaStreamDestroy(sst);
     for (int i = 0; i < n_tasks; i++) {
         results[i].cpu_mode = (cpu_mode == RTGPU_EXEC_CPU_FP_ONE_CORE && fifo_fail == 0)
                                   ? RTGPU_EXEC_CPU_FP_ONE_CORE : RTGPU_EXEC_CPU_PARALLEL;

@@ -10,7 +10,7 @@
  * numerators / denominators (or ints), ExecBounds.lo / .hi,
  * GpuKernelModel.work / .critical_path_overhead / .interleave_ratio.
  *
- *   pack(tasksets) -> (blobs: bytes of int64, set_off: bytes, task_base:
+ *   pack(tasksets, compact=False) -> (blobs: bytes of int64, set_off: bytes, task_base:
  *                      bytes, scales: list[int], orders: list[tuple[TaskSpec]]
  *                      -- each set's task objects in blob order)
  *
@@ -23,6 +23,7 @@
 #include <structmember.h>
 
 #include <stdint.h>
+#include <string.h>
 
 #include <algorithm>
 #include <numeric>
@@ -155,6 +156,7 @@ struct Scratch {
     std::vector<Frac> arena;
     std::vector<int> order;
     PyObject *hold = nullptr; /* the current set's task sequence (owns tf[].obj) */
+    int compact = 0;          /* emit compact blobs where the values fit */
     ~Scratch() { Py_XDECREF(hold); }
 };
 
@@ -226,6 +228,24 @@ bool read_task(PyObject *t, TaskF &r, std::vector<Frac> &ar, int mem_model) {
  * Python-level property) is read once per distinct member */
 PyObject *g_last_mm = nullptr;
 int g_last_mm_code = 0;
+
+/* the set at words[base..] in the compact form (int32 segment areas, header
+ * word 7 = 1) when every segment value fits int32, as tests/blobtools.compact */
+void compact_set(std::vector<int64_t> &words, size_t base) {
+    int64_t *h = words.data() + base;
+    const int64_t n = h[0], hb = 8 + 8 * n, W = (int64_t)(words.size() - base);
+    for (int64_t j = hb; j < W; j++)
+        if (h[j] < INT32_MIN || h[j] > INT32_MAX) return;
+    const int64_t nseg = W - hb;
+    std::vector<int32_t> seg(nseg + (nseg & 1), 0);
+    for (int64_t j = 0; j < nseg; j++) seg[j] = (int32_t)h[hb + j];
+    for (int64_t r = 0; r < n; r++) h[8 + 8 * r + 5] = 2 * hb + (h[8 + 8 * r + 5] - hb);
+    const int64_t W2 = hb + (int64_t)seg.size() / 2;
+    memcpy(h + hb, seg.data(), seg.size() * sizeof(int32_t));
+    h[7] = 1;
+    h[4] = W2;
+    words.resize(base + (size_t)W2);
+}
 
 bool pack_one(PyObject *ts, Scratch &sc, std::vector<int64_t> &words, int64_t &scale) {
     PyObject *tasks_o = PyObject_GetAttr(ts, s_tasks);
@@ -332,12 +352,14 @@ bool pack_one(PyObject *ts, Scratch &sc, std::vector<int64_t> &words, int64_t &s
         seg_off += 2 * m + 2 * p + 4 * g;
     }
     scale = S;
+    if (sc.compact) compact_set(words, base);
     return true;
 }
 
 PyObject *py_pack(PyObject *, PyObject *args) {
     PyObject *seq_o;
-    if (!PyArg_ParseTuple(args, "O", &seq_o)) return nullptr;
+    int compact = 0;
+    if (!PyArg_ParseTuple(args, "O|p", &seq_o, &compact)) return nullptr;
     PyObject *seq = PySequence_Fast(seq_o, "pack expects a sequence of TaskSets");
     if (!seq) return nullptr;
     const Py_ssize_t S = PySequence_Fast_GET_SIZE(seq);
@@ -346,6 +368,7 @@ PyObject *py_pack(PyObject *, PyObject *args) {
     set_off.reserve((size_t)S + 1);
     task_base.reserve((size_t)S + 1);
     Scratch sc;
+    sc.compact = compact;
     PyObject *scales = PyList_New(S), *orders = PyList_New(S);
     bool ok = scales && orders;
     for (Py_ssize_t s = 0; ok && s < S; s++) {

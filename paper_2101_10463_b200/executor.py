@@ -200,6 +200,12 @@ class WcrtReport:
     # one partition's, or GPU-wide?
     overruns: list = field(default_factory=list)
     launch_ratio_pcts: dict = field(default_factory=dict)  # span / GR_up percentiles over all launches
+    # the stall sentinel (an SM outside every partition reading %globaltimer):
+    # GPU pauses during the run, and every launch's span with the paused time
+    # it overlapped taken out -- Lemma 4 bounds execution, not platform pauses
+    stalls: dict = field(default_factory=dict)
+    max_kernel_ratio_net: Optional[float] = None
+    kernels_within_bound_net: Optional[bool] = None
 
 
 def _ceil_margin(x_us: float, margin: float) -> int:
@@ -258,8 +264,27 @@ def launch_log():
              "mhz": buf[7 * k + 6]} for k in range(n)]
 
 
-def _overrun_context(log, grs_of, limit: int = 12):
-    """Launches over their bound and what ran beside them."""
+def stall_log():
+    """The last run's stall sentinel (rtgpu_exec_stall_log): (sentinel SM or
+    None, [(start_us, end_us), ...] intervals over 50 us in which an SM no
+    task used did not execute), in the launch log's %globaltimer time base."""
+    L = _lib()
+    L.rtgpu_exec_stall_log.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int)]
+    sm = ctypes.c_int(-1)
+    n = L.rtgpu_exec_stall_log(None, 0, ctypes.byref(sm))
+    buf = (ctypes.c_double * (2 * max(n, 1)))()
+    n = L.rtgpu_exec_stall_log(buf, n, ctypes.byref(sm))
+    return (None if sm.value < 0 else sm.value), [(buf[2 * k], buf[2 * k + 1]) for k in range(n)]
+
+
+def _stalled_us(t0: float, t1: float, stalls) -> float:
+    return sum(max(0.0, min(t1, b) - max(t0, a)) for a, b in stalls)
+
+
+def _overrun_context(log, grs_of, limit: int = 12, stalls=None):
+    """Launches over their bound, the sentinel's paused time inside them, and
+    what ran beside them."""
     ratio = lambda e: e["span_us"] / grs_of[e["task"]][e["seg"]]  # noqa: E731
     out = []
     for e in sorted((e for e in log if ratio(e) > 1.0), key=ratio, reverse=True)[:limit]:
@@ -268,6 +293,7 @@ def _overrun_context(log, grs_of, limit: int = 12):
                    "overlap_us": round(min(a1, o["t0_us"] + o["span_us"]) - max(a0, o["t0_us"]), 1)}
                   for o in log if o is not e and o["t0_us"] < a1 and o["t0_us"] + o["span_us"] > a0]
         out.append({"task": e["task"], "seg": e["seg"], "ratio": round(ratio(e), 3),
+                    "stalled_us": round(_stalled_us(a0, a1, stalls), 1) if stalls is not None else None,
                     "span_us": round(e["span_us"], 1), "t0_ms": round((a0 - log[0]["t0_us"]) * 1e-3, 3),
                     "items": e["items"], "mhz": round(e["mhz"]), "beside": beside})
     return out
@@ -469,8 +495,20 @@ def wcrt_experiment(n_tasks: int = 4, m: int = 3, iters: int = 2048, seed: int =
     grs_of = [[float(gpu_response_bounds(g, 2 * len(sms)).hi) for g in s.gpu_segments]
               for s, sms in zip(specs, parts)]
     log = launch_log()
+    sentinel, stalls = stall_log()
+    if log and sentinel is not None:
+        net = [(e["span_us"] - _stalled_us(e["t0_us"], e["t0_us"] + e["span_us"], stalls))
+               / grs_of[e["task"]][e["seg"]] for e in log]
+        out.max_kernel_ratio_net = round(max(net), 4)
+        out.kernels_within_bound_net = bool(max(net) <= 1.0)
+        dur = [b - a for a, b in stalls]
+        out.stalls = {"sentinel_sm": sentinel, "count": len(stalls),
+                      "max_us": round(max(dur), 1) if dur else 0.0,
+                      "total_us": round(sum(dur), 1),
+                      "launches_overlapping": sum(1 for e in log if _stalled_us(
+                          e["t0_us"], e["t0_us"] + e["span_us"], stalls) > 0)}
     if log:
-        out.overruns = _overrun_context(log, grs_of)
+        out.overruns = _overrun_context(log, grs_of, stalls=stalls if sentinel is not None else None)
         rs = np.array([e["span_us"] / grs_of[e["task"]][e["seg"]] for e in log])
         out.launch_ratio_pcts = {"launches": len(rs), "p50": round(float(np.percentile(rs, 50)), 3),
                                  "p99": round(float(np.percentile(rs, 99)), 3),

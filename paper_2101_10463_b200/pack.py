@@ -216,7 +216,7 @@ def pack_set(ts: TaskSet) -> tuple[list[int], int, tuple]:
     return blob, S, order
 
 
-def pack_tasksets(tasksets: Sequence[TaskSet]) -> PackedBatch:
+def pack_tasksets(tasksets: Sequence[TaskSet], compact: bool = False) -> PackedBatch:
     """The batch of blobs: the native packer (csrc/packer.cpp, the same
     words) when built; a set it refuses (values beyond int64, a shape the
     engine does not take) is packed by pack_set for the exact exception."""
@@ -226,7 +226,7 @@ def pack_tasksets(tasksets: Sequence[TaskSet]) -> PackedBatch:
         _packer = None
     if _packer is not None and tasksets:
         try:
-            b, so, tb, scales, orders = _packer.pack(tasksets)
+            b, so, tb, scales, orders = _packer.pack(tasksets, compact)
         except (ValueError, OverflowError, TypeError, AttributeError):
             pass
         else:

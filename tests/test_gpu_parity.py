@@ -255,3 +255,23 @@ def test_e2e_no_stream_override_matches_streamed(tmp_path):
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def _no_detail(d):
+    return {**d, "per_task": {k: {**v, "gpu_r": [], "mem_r_up": [], "cpu_r_up": []}
+                              for k, v in d["per_task"].items()}}
+
+
+@pytest.mark.parametrize("fixture", ["rtgpu_golden.json", "ood_golden.json"])
+@pytest.mark.parametrize("mi", [0, 1, 2])
+def test_batch_without_detail_matches_reference(fixture, mi):
+    """analyze_batch(detail=False) packs compact blobs (the fast / lattice
+    kernels' form, csrc/packer.cpp compact_set): verdicts, allocations and
+    end-to-end bounds equal the reference's reports, in and out of the
+    reference's validation domain."""
+    method = METHODS[mi]
+    cases = [c for c in load_cases(fixture) if "raises" not in c[method.value]]
+    reps = analyze_batch([ts_from_exact(c["taskset"]) for c in cases], method, detail=False)
+    bad = [s for s, (c, r) in enumerate(zip(cases, reps))
+           if report_to_dict(r) != _no_detail(c[method.value])]
+    assert not bad, bad[:8]

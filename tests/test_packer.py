@@ -43,3 +43,16 @@ def test_native_equals_python_generated(n, m, u, mm):
                    mem_model=MemModel(mm), lo_frac=Fraction(7, 10))
     sets = [generate_taskset(gp, i) for i in range(200)]
     same(pack_tasksets(sets), pack_tasksets_py(sets))
+
+
+def test_native_compact_equals_compacted_python():
+    """pack(compact=True) writes tests/blobtools.compact's words: int32 segment
+    areas wherever every value of the set fits, int64 elsewhere."""
+    from blobtools import compact
+    gp = GenParams(n_tasks=6, n_subtasks=4, target_utilization=Fraction(1, 2))
+    sets = [generate_taskset(gp, f"c{i}") for i in range(30)]
+    want = pack_tasksets_py(sets)
+    cb, co, ct = compact(want.blobs, want.set_off, want.task_base)
+    got = pack_tasksets(sets, compact=True)
+    assert np.array_equal(got.blobs, cb) and np.array_equal(got.set_off, co)
+    assert np.array_equal(got.task_base, ct)
