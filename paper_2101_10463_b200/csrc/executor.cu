@@ -186,12 +186,14 @@ struct StallGap {
 };
 
 __global__ void stall_sentinel(unsigned target_sm, const volatile int *stop, int *claim, StallGap *gaps,
-                               unsigned *ngaps, unsigned cap, unsigned long long thresh_ns) {
+                               unsigned *ngaps, unsigned cap, unsigned long long thresh_ns,
+                               unsigned long long max_ns) {
     if (smid() != target_sm || threadIdx.x != 0) return;
     if (atomicCAS(claim, 0, 1) != 0) return;
     unsigned long long prev = gtimer();
+    const unsigned long long t_end = prev + max_ns; /* never outlives the run by much */
     for (unsigned it = 0;; it++) {
-        if ((it & 63) == 0 && *stop) break;
+        if ((it & 63) == 0 && (*stop || prev > t_end)) break;
         __nanosleep(2000);
         const unsigned long long now = gtimer();
         if (now - prev > thresh_ns) {
@@ -812,7 +814,7 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
         cudaMemsetAsync(sbuf, 0, 64, sst);
         stall_sentinel<<<2 * nsm, 32, 0, sst>>>((unsigned)free_sm, (const volatile int *)sbuf, (int *)(sbuf + 4),
                                                 (StallGap *)(sbuf + 64), (unsigned *)(sbuf + 8), STALL_CAP,
-                                                50000ull);
+                                                50000ull, (unsigned long long)((horizon_us + 30e6) * 1e3));
     } else {
         free_sm = -1;
     }
@@ -936,8 +938,14 @@ int rtgpu_exec_run(const rtgpu_exec_task *tasks, int n_tasks, double horizon_us,
         g_stalls.clear();
         g_sentinel_sm = free_sm;
         if (free_sm >= 0) {
+            /* the stop flag goes through a second stream: sst is occupied by
+             * the sentinel itself until it sees the flag */
             static const int one = 1;
-            cudaMemcpyAsync(sbuf, &one, sizeof one, cudaMemcpyHostToDevice, sst);
+            cudaStream_t s2 = nullptr;
+            cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+            cudaMemcpyAsync(sbuf, &one, sizeof one, cudaMemcpyHostToDevice, s2);
+            cudaStreamSynchronize(s2);
+            cudaStreamDestroy(s2);
             unsigned n = 0;
             cudaMemcpyAsync(&n, sbuf + 8, sizeof n, cudaMemcpyDeviceToHost, sst);
             cudaStreamSynchronize(sst);
