@@ -288,11 +288,16 @@ def analyze_arrays(a: TaskArrays, method: AnalysisMethod = AnalysisMethod.RTGPU,
     end-to-end bound) of S same-shape sets in one engine call: the batch form
     of analyze_rtgpu / the baselines (reference analysis.py:275, :319, :355).
     budget <= 0: unlimited allocation search."""
+    S, n, _ = a.shape
+    if S == 0:
+        a.check()
+        z = np.zeros((0, n), np.int64)
+        return ArrayReport(np.zeros(0, np.int32), np.zeros((0, n), np.int32), z if bounds else None,
+                           z.copy() if bounds else None, np.zeros(0, np.int64))
     pk = pack_arrays(a)
     flags = F_BOUNDS if bounds else 0
     res = engine.analyze_packed(pk.blobs, pk.set_off, pk.task_base, METHOD_CODES[AnalysisMethod(method)],
                                 flags, budget)
-    S, n, _ = a.shape
     inv = np.argsort(pk.order, axis=1)  # caller task i sits at blob position inv[s, i]
 
     def caller(x):

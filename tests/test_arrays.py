@@ -154,3 +154,10 @@ def test_analyze_arrays_matches_object_api():
         for i in range(8):
             if f"t{i}" in r.per_task:
                 assert rep.end_to_end(k, i) == r.per_task[f"t{i}"].end_to_end_up, (k, i)
+
+
+def test_empty_batch():
+    a = random_arrays(0, 4, 3)
+    assert pack_arrays(a).n_sets == 0
+    rep = analyze_arrays(a, bounds=True)
+    assert rep.status.shape == (0,) and rep.vsm.shape == (0, 4) and rep.e2e_num.shape == (0, 4)
