@@ -529,6 +529,12 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
         }
         cudaMemcpyAsync(h_over, p.ctr + 6, 8, cudaMemcpyDeviceToHost, cs);
         cudaMemcpyAsync(h_over + 1, q.chunk_abort, 8, cudaMemcpyDeviceToHost, cs);
+        /* the results go out behind them without a host round trip; the
+         * rare oversize / abort cases below overwrite them */
+        cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, cs);
+        cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, cs);
+        cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, cs);
+        if (trace) cudaEventRecord(tev[5], cs);
         cudaError_t e = cudaStreamSynchronize(cs);
         if (e != cudaSuccess) {
             set_err("rtgpu_analyze_host", e);
@@ -555,15 +561,14 @@ int rtgpu_analyze_host(const int64_t *blobs, const int64_t *set_off, const int64
                 r.esc[2] = p.esc[0]; /* free now */
                 rc = launch_general(r, cs);
                 if (rc) return rc;
-            }
-            cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, cs);
-            cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, cs);
-            cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, cs);
-            if (trace) cudaEventRecord(tev[5], cs);
-            e = cudaStreamSynchronize(cs);
-            if (e != cudaSuccess) {
-                set_err("rtgpu_analyze_host", e);
-                return -8;
+                cudaMemcpyAsync(status, g_h_status.p, n_sets * 4, cudaMemcpyDeviceToHost, cs);
+                cudaMemcpyAsync(evals, g_h_evals.p, n_sets * 8, cudaMemcpyDeviceToHost, cs);
+                cudaMemcpyAsync(vsm, g_h_vsm.p, T * 4, cudaMemcpyDeviceToHost, cs);
+                e = cudaStreamSynchronize(cs);
+                if (e != cudaSuccess) {
+                    set_err("rtgpu_analyze_host", e);
+                    return -8;
+                }
             }
             if (trace) {
                 float t[6] = {0};
