@@ -2052,11 +2052,24 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         V bmax_k = 0;
         if (t.p > 0) {
             i64 bmax_t = 0, bsum_t = 0;
+#if defined(__CUDA_ARCH__) && defined(RTGPU_FAST_LANESUMS)
+            { /* A/B: one load per lane and two butterflies (p <= 30) */
+                const i64 v = tm.lane < t.p ? ml_hi[tm.lane] + t.B : 0;
+                bmax_t = v;
+                bsum_t = v;
+                #pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    bmax_t = tmax(bmax_t, shfl_x(bmax_t, off));
+                    bsum_t += shfl_x(bsum_t, off);
+                }
+            }
+#else
             #pragma unroll 1
             for (int j = 0; j < t.p; j++) {
                 bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
                 bsum_t += ml_hi[j] + t.B;
             }
+#endif
             const V bmax = Num<V>::sc(bmax_t, q);
             bsum_k = bsum_t;
             bmax_k = bmax;

@@ -828,6 +828,30 @@ RT_HD i64 lat_chain_sum(const TM &tm, const LCtx &c, const LKey &key, int cnt, i
     return sum;
 }
 
+/* max and sum of ml[j] + B over the p copies of a task: one load per lane
+ * and two butterflies on a team (p <= 30), a loop in the host harness */
+#ifdef __CUDACC__
+template <int W>
+__device__ __forceinline__ void lat_copy_sums(const LTeam<W> &tm, Seg32 ml, int p, i64 B, i64 &mx, i64 &sm) {
+    const i64 v = tm.lane < p ? (i64)ml[tm.lane] + B : 0;
+    mx = v;
+    sm = v;
+    #pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        mx = tmax(mx, shfl_x(mx, off));
+        sm += shfl_x(sm, off);
+    }
+}
+#endif
+RT_HD void lat_copy_sums(const LSeq &, Seg32 ml, int p, i64 B, i64 &mx, i64 &sm) {
+    mx = 0;
+    sm = 0;
+    for (int j = 0; j < p; j++) {
+        mx = tmax(mx, (i64)ml[j] + B);
+        sm += ml[j] + B;
+    }
+}
+
 /* GR up of task i at count g (gpu.py:25 summed over its kernels) as
  * bi + bf / d, d = 2 A g */
 RT_HD LBase lat_grup(const LCtx &c, int i, int g) {
@@ -840,8 +864,29 @@ RT_HD LBase lat_grup(const LCtx &c, int i, int g) {
     }
     r.d = 2 * c.A * (i64)g;
     const i64 infl = c.sInfl()[i];
-    r.bi = c.sGL()[i] + infl / r.d;
-    r.bf = infl % r.d;
+    i64 q, rem;
+#ifdef RTGPU_LAT_FPQ
+    if (infl >= 0 && infl < ((i64)1 << 53)) {
+#else
+    if (false) {
+#endif
+        /* FP64 quotient (both operands exact) and one correction step: no
+         * 64-bit integer division on the search's path */
+        q = (i64)floor((double)infl / (double)r.d);
+        rem = infl - q * r.d;
+        if (rem < 0) {
+            q--;
+            rem += r.d;
+        } else if (rem >= r.d) {
+            q++;
+            rem -= r.d;
+        }
+    } else {
+        q = infl / r.d;
+        rem = infl % r.d;
+    }
+    r.bi = c.sGL()[i] + q;
+    r.bf = rem;
     return r;
 }
 
@@ -1021,11 +1066,15 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         bool rmax_exact = true;
         if (p > 0) {
             i64 bmax = 0;
+#ifdef RTGPU_LAT_LANESUMS
+            lat_copy_sums(tm, ml_hi, p, B, bmax, bsum);
+#else
             #pragma unroll 1
             for (int j = 0; j < p; j++) {
                 bmax = tmax(bmax, (i64)ml_hi[j] + B);
                 bsum += ml_hi[j] + B;
             }
+#endif
             lbm = {bmax, 0, 1};
             double r = -1.0;
 #ifndef RTGPU_LAT_NOGUESS
