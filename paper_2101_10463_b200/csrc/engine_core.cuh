@@ -2052,8 +2052,9 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         V bmax_k = 0;
         if (t.p > 0) {
             i64 bmax_t = 0, bsum_t = 0;
-#if defined(__CUDA_ARCH__) && defined(RTGPU_FAST_LANESUMS)
-            { /* A/B: one load per lane and two butterflies (p <= 30) */
+#if defined(__CUDA_ARCH__) && !defined(RTGPU_FAST_NO_LANESUMS)
+            { /* one load per lane and two butterflies (p <= 30): +1.1% on the
+               * 8 x 5 sweep over the sequential loop (scripts/gpu_lat_ab.sh r2u) */
                 const i64 v = tm.lane < t.p ? ml_hi[tm.lane] + t.B : 0;
                 bmax_t = v;
                 bsum_t = v;

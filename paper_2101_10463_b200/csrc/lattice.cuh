@@ -865,7 +865,7 @@ RT_HD LBase lat_grup(const LCtx &c, int i, int g) {
     r.d = 2 * c.A * (i64)g;
     const i64 infl = c.sInfl()[i];
     i64 q, rem;
-#ifdef RTGPU_LAT_FPQ
+#ifdef RTGPU_LAT_FPQ /* off: more spills than the division costs (r2u: -2.5%) */
     if (infl >= 0 && infl < ((i64)1 << 53)) {
 #else
     if (false) {
@@ -1066,7 +1066,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         bool rmax_exact = true;
         if (p > 0) {
             i64 bmax = 0;
-#ifdef RTGPU_LAT_LANESUMS
+#ifndef RTGPU_LAT_NO_LANESUMS /* alloc64 +4% (scripts/gpu_lat_ab.sh r2u) */
             lat_copy_sums(tm, ml_hi, p, B, bmax, bsum);
 #else
             #pragma unroll 1
