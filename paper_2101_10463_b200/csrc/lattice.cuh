@@ -134,13 +134,42 @@ RT_HD int li_flags(int w) { return w >> 20; }
 
 /* Typed access to a team's slab: on the device addressed from the dynamic
  * shared-memory symbol (LDS/STS), in the host harness from a heap buffer. */
+/* On the device one copy of the slab geometry per CTA sits at the start of
+ * dynamic shared memory (LSLAB_HDR bytes, before the teams' slabs): read
+ * from there at every use, the offsets never occupy registers across the
+ * out-of-line fixed points (they were a third of the kernel's stack frame). */
+#define LSLAB_HDR 128
+static_assert(sizeof(LSlab) <= LSLAB_HDR, "slab header");
+#ifdef __CUDACC__
+__device__ __forceinline__ const LSlab &lslab_dev() { return *(const LSlab *)rt_dyn_smem; }
+#endif
+
+/* The warp-uniform state of one set's allocation search (lattice_set): one
+ * per warp in shared memory on the device, after the slab header. */
+struct LSt {
+    LBase mw, cw, lbm;
+    double mwN, cwN, mg;
+    i64 used, rest_min, evals, mr_ub, sum_mr, bsum, sum_cr;
+    int k, st, glo, ghi, g, lo, hi, phase, cand, fail, rmax_exact, pass;
+};
+#define LST_BYTES ((int)((sizeof(LSt) + 15) & ~(size_t)15))
+
 struct LCtx {
     unsigned char *hbase; /* host harness only */
     int base;             /* byte offset of the slab */
-    LSlab L;
+    int sto;              /* byte offset of the warp's LSt (device) */
+    LSt *sth;             /* the LSt (host harness) */
+    LSlab Lh;             /* host harness only */
     const i64 *blob;
     int n, GN, mm;
     i64 A;
+    RT_HD const LSlab &L() const {
+#ifdef __CUDA_ARCH__
+        return lslab_dev();
+#else
+        return Lh;
+#endif
+    }
     RT_HD unsigned char *sb() const {
 #ifdef __CUDA_ARCH__
         return rt_dyn_smem + base;
@@ -148,22 +177,29 @@ struct LCtx {
         return hbase + base;
 #endif
     }
-    RT_HD i64 *D() const { return (i64 *)(sb() + L.o_D); }
-    RT_HD i64 *sClu() const { return (i64 *)(sb() + L.o_sClu); }
-    RT_HD i64 *sInfl() const { return (i64 *)(sb() + L.o_sInfl); }
-    RT_HD i64 *sGL() const { return (i64 *)(sb() + L.o_sGL); }
-    RT_HD i64 *B() const { return (i64 *)(sb() + L.o_B); }
-    RT_HD double *S() const { return (double *)(sb() + L.o_s); }
-    RT_HD double *IS() const { return (double *)(sb() + L.o_invs); }
-    RT_HD int *seg() const { return (int *)(sb() + L.o_seg); }
-    RT_HD int *gmin() const { return (int *)(sb() + L.o_gmin); }
-    RT_HD int *g() const { return (int *)(sb() + L.o_g); }
-    RT_HD int *info() const { return (int *)(sb() + L.o_info); }
-    RT_HD int *hpn() const { return (int *)(sb() + L.o_hpn); }
-    RT_HD double *VC() const { return (double *)(sb() + L.o_vc); }
-    RT_HD double *VM() const { return (double *)(sb() + L.o_vm); }
-    RT_HD i64 *bases() const { return (i64 *)(sb() + L.o_bases); }
-    RT_HD int *ord() const { return (int *)(sb() + L.o_ord); }
+    RT_HD LSt *stp() const {
+#ifdef __CUDA_ARCH__
+        return (LSt *)(rt_dyn_smem + sto);
+#else
+        return sth;
+#endif
+    }
+    RT_HD i64 *D() const { return (i64 *)(sb() + L().o_D); }
+    RT_HD i64 *sClu() const { return (i64 *)(sb() + L().o_sClu); }
+    RT_HD i64 *sInfl() const { return (i64 *)(sb() + L().o_sInfl); }
+    RT_HD i64 *sGL() const { return (i64 *)(sb() + L().o_sGL); }
+    RT_HD i64 *B() const { return (i64 *)(sb() + L().o_B); }
+    RT_HD double *S() const { return (double *)(sb() + L().o_s); }
+    RT_HD double *IS() const { return (double *)(sb() + L().o_invs); }
+    RT_HD int *seg() const { return (int *)(sb() + L().o_seg); }
+    RT_HD int *gmin() const { return (int *)(sb() + L().o_gmin); }
+    RT_HD int *g() const { return (int *)(sb() + L().o_g); }
+    RT_HD int *info() const { return (int *)(sb() + L().o_info); }
+    RT_HD int *hpn() const { return (int *)(sb() + L().o_hpn); }
+    RT_HD double *VC() const { return (double *)(sb() + L().o_vc); }
+    RT_HD double *VM() const { return (double *)(sb() + L().o_vm); }
+    RT_HD i64 *bases() const { return (i64 *)(sb() + L().o_bases); }
+    RT_HD int *ord() const { return (int *)(sb() + L().o_ord); }
     RT_HD Seg32 segs(int i) const { return Seg32{(const int32_t *)blob + seg()[i]}; }
 };
 
@@ -324,9 +360,9 @@ RT_HD LKey lat_key(const LCtx &c, int k, int res) {
     LKey q;
     q.hbase = c.hbase;
     q.base = c.base;
-    q.maxn = c.L.maxn;
-    q.MC = c.L.MC;
-    q.MP = c.L.MP;
+    q.maxn = c.L().maxn;
+    q.MC = c.L().MC;
+    q.MP = c.L().MP;
     q.task = k;
     q.res = res;
     return q;
@@ -336,15 +372,15 @@ RT_HD LChains lat_chains(const LCtx &c, int k, int res, int W) {
     LChains ch;
     ch.hbase = c.hbase;
     ch.base = c.base;
-    ch.o_s = c.L.o_s;
-    ch.o_invs = c.L.o_invs;
-    ch.o_info = c.L.o_info;
-    ch.o_red = c.L.o_red;
+    ch.o_s = c.L().o_s;
+    ch.o_invs = c.L().o_invs;
+    ch.o_info = c.L().o_info;
+    ch.o_red = c.L().o_red;
     ch.k = c.hpn()[k];
     ch.res = res;
-    ch.PM = res == K_CPU ? c.L.MC : c.L.MP;
-    ch.stride = res == K_CPU ? c.L.SC : c.L.SM;
-    ch.vbase = res == K_CPU ? c.L.o_vc : c.L.o_vm;
+    ch.PM = res == K_CPU ? c.L().MC : c.L().MP;
+    ch.stride = res == K_CPU ? c.L().SC : c.L().SM;
+    ch.vbase = res == K_CPU ? c.L().o_vc : c.L().o_vm;
     ch.lg = lat_lg(ch.k, ch.PM, W);
     int hf = 1;
     while (2 * hf < ch.PM) hf <<= 1;
@@ -550,9 +586,11 @@ RT_HD double lfp_lat_body(const TM &tm, const LKey key, const LBase b, double N,
     LCtx c;
     c.hbase = key.hbase;
     c.base = key.base;
-    c.L.init(Dims{key.maxn, key.MC, key.MP});
+#ifndef __CUDA_ARCH__
+    c.Lh.init(Dims{key.maxn, key.MC, key.MP});
+#endif
     const LChains ch = lat_chains(c, key.task, key.res, tm.width());
-    RT_COUNT(g_cnt_flfp[ch.res]);
+    RT_COUNT(g_cnt_flfp[4 + ch.res + 2 * mode]);
     if (lb_over(b, N, D)) return -1.0;
     const double invd = b.bf ? lat_rcp(b.d) : 0.0;
     typename TM::Cache cache;
@@ -563,14 +601,14 @@ RT_HD double lfp_lat_body(const TM &tm, const LKey key, const LBase b, double N,
          * return floor(I(r)), the offset of f(r) rounded down to the
          * lattice, or -1 when not verified.  I(r) = q + F, F the exact sum
          * of the fractional parts (FP64 a.f within 1e-9 of it). */
-        RT_COUNT(g_cnt_fit[ch.res]);
+        RT_COUNT(g_cnt_fit[6 + ch.res]);
         const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd, tm.cache_ptr(cache), false);
         const double ub = floor(a.q + a.f + 1e-6);
         return (a.q + a.f + 1e-6 <= N) ? ub : -1.0;
     }
     #pragma unroll 1
     for (int it = 0; it < ITER_CAP; it++) {
-        RT_COUNT(g_cnt_fit[ch.res]);
+        RT_COUNT(g_cnt_fit[4 + ch.res]);
         const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd, tm.cache_ptr(cache));
         if (!a.nonint && a.q <= N) return N; /* f(r) <= r with r <= lfp: r is the lfp */
         double Nn = a.q + ceil(a.f - 1e-6);
@@ -604,7 +642,7 @@ RT_HD i64 lat_load(const LCtx &c, int i) {
     c.g()[i] = 0;
     c.gmin()[i] = 0;
     c.B()[i] = 0;
-    if (m < 1 || m > c.L.MC || p != want_p || p > c.L.MP || T <= 0 || D <= 0 || D > T || T >= ((i64)1 << 56) ||
+    if (m < 1 || m > c.L().MC || p != want_p || p > c.L().MP || T <= 0 || D <= 0 || D > T || T >= ((i64)1 << 56) ||
         c.A >= (1 << 16) || r[5] < 0 || r[5] > (1 << 30)) {
         c.info()[i] = (m & 0xff) | (p & 0xff) << 8 | TF_UNSUP << 20;
         return 0;
@@ -741,16 +779,16 @@ RT_HD void lat_view_lane(const LCtx &c, int i, int lane) {
         Cm = (double)T * ds - (two ? 0.0 : (double)gw_lo[m - 2]);
         Fm = (double)(T - D + cl_lo[m - 1] + cl_lo[0]) * ds + (two ? 0.0 : (double)gw_lo[m - 2]);
     }
-    double *vc = c.VC() + (size_t)i * c.L.SC;
-    double *vm = c.VM() + (size_t)i * c.L.SM;
+    double *vc = c.VC() + (size_t)i * c.L().SC;
+    double *vm = c.VM() + (size_t)i * c.L().SM;
     if (lane >= 0) {
         double e = 0, gap = 0;
         if (lane < m) cpu_seg(lane, e, gap);
-        lat_build_chain(vc, c.L.MC, m, lane, e, gap, Cc, Fc);
+        lat_build_chain(vc, c.L().MC, m, lane, e, gap, Cc, Fc);
         if (p > 0) {
             e = gap = 0;
             if (lane < p) mem_seg(lane, e, gap);
-            lat_build_chain(vm, c.L.MP, p, lane, e, gap, Cm, Fm);
+            lat_build_chain(vm, c.L().MP, p, lane, e, gap, Cm, Fm);
         }
         return;
     }
@@ -771,8 +809,8 @@ RT_HD void lat_view_lane(const LCtx &c, int i, int lane) {
         v[2 * PM + 2] = P + first;
         v[2 * PM + 3] = 1.0 / C;
     };
-    seq(vc, c.L.MC, m, true, Cc, Fc);
-    if (p > 0) seq(vm, c.L.MP, p, false, Cm, Fm);
+    seq(vc, c.L().MC, m, true, Cc, Fc);
+    if (p > 0) seq(vm, c.L().MP, p, false, Cm, Fm);
 }
 
 #ifdef __CUDACC__
@@ -973,11 +1011,11 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
     c.mm = (int)h[2];
     c.A = A;
     evals = 0;
-    if (h[7] != 1 || n < 1 || n > c.L.maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > (1 << 20))
+    if (h[7] != 1 || n < 1 || n > c.L().maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > (1 << 20))
         return ST_ESCALATE;
     /* loads; each task's range bound parks in its (not yet built) CPU view */
     tm.pfor(n, [&](int i) {
-        *(i64 *)(c.VC() + (size_t)i * c.L.SC) = lat_load(c, i);
+        *(i64 *)(c.VC() + (size_t)i * c.L().SC) = lat_load(c, i);
         vsm[i] = 0;
         if (bounds) {
             e2e[i] = RTGPU_ABSENT;
@@ -994,7 +1032,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         if (fl & (TF_UNSUP | TF_IRREG | TF_INV)) return ST_ESCALATE;
         if (fl & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE; /* empty report */
         if (li_gpu(info[k])) need += c.gmin()[k];
-        vb_max = tmax(vb_max, *(const i64 *)(c.VC() + (size_t)k * c.L.SC));
+        vb_max = tmax(vb_max, *(const i64 *)(c.VC() + (size_t)k * c.L().SC));
         if (k > 0 && rec[RTGPU_TASK_WORDS * k + 4] < rec[RTGPU_TASK_WORDS * (k - 1) + 4]) return ST_ESCALATE;
     }
     if (need > GN) return RTGPU_UNSCHEDULABLE; /* no allocation at all: empty report */
@@ -1004,7 +1042,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         if (li_gpu(info[k])) gtop = tmax(gtop, (int)tmin((i64)GN, (i64)c.gmin()[k] + (GN - need)));
     /* every value at any scale s_i <= 2 gtop below 2^51 (room for the
      * half-tick marker); the window fraction bf * s_i below 2^52 */
-    if ((i128)vb_max * range_factor(n, c.L.MC, c.L.MP) * (2 * gtop) >= ((i128)1 << 51)) return ST_ESCALATE;
+    if ((i128)vb_max * range_factor(n, c.L().MC, c.L().MP) * (2 * gtop) >= ((i128)1 << 51)) return ST_ESCALATE;
     if ((i128)4 * A * gtop * gtop >= ((i128)1 << 52)) return ST_ESCALATE;
     /* hp(k) = [0, first index of k's priority); blocking term of
      * analysis.py:162 = longest copy of a lower-priority task (B[] holds each
@@ -1019,39 +1057,47 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         #pragma unroll 1
         for (int i = k + 1; i < n; i++)
             if (rec[RTGPU_TASK_WORDS * i + 4] > pk) b = tmax(b, c.B()[i]);
-        *(i64 *)(c.VC() + (size_t)k * c.L.SC) = b;
+        *(i64 *)(c.VC() + (size_t)k * c.L().SC) = b;
     });
-    tm.pfor(n, [&](int k) { c.B()[k] = *(const i64 *)(c.VC() + (size_t)k * c.L.SC); });
+    tm.pfor(n, [&](int k) { c.B()[k] = *(const i64 *)(c.VC() + (size_t)k * c.L().SC); });
     (void)bases;
-    i64 used = 0, rest_min = need;
+    /* The search state is warp-uniform and lives in the warp's LSt in shared
+     * memory (every lane stores the same value): across the out-of-line fixed
+     * points it is reloaded from there instead of being spilled per lane to
+     * a stack frame that does not fit L1 (the r2w profile: 60% of the
+     * control code's stall samples waited on local loads missing to L2).
+     * Per-task values are re-read from the slab's task records at use. */
+    LSt &S = *c.stp();
+    S.used = 0;
+    S.rest_min = need;
     /* warm starts: the last converged memory / CPU fixed point (base, N);
      * valid for any later task (hp(k) only grows) at a base >= its base */
-    LBase mw = {-1, 0, 1}, cw = {-1, 0, 1};
-    double mwN = 0, cwN = 0;
-    double mg = -1.0; /* the last task's memory offset (or its verified bound): the next guess */
-    int st = RTGPU_SCHEDULABLE;
-    const int W = tm.width();
+    S.mw = LBase{-1, 0, 1};
+    S.cw = LBase{-1, 0, 1};
+    S.mwN = 0;
+    S.cwN = 0;
+    S.mg = -1.0; /* the last task's memory offset (or its verified bound): the next guess */
+    S.st = RTGPU_SCHEDULABLE;
+    S.evals = 0;
     #pragma unroll 1
-    for (int k = 0; k < n; k++) {
-        if (k > 0) lat_view(tm, c, k - 1); /* counts of tasks before k are final */
-        const int inf = info[k];
-        const int m = li_m(inf), p = li_p(inf);
-        const bool gpu = li_gpu(inf);
-        const i64 D = c.D()[k], B = c.B()[k], sClu = c.sClu()[k];
-        const Seg32 sg = c.segs(k);
-        const Seg32 cl_hi = sg + m, ml_hi = sg + 2 * m + p;
-        const LKey chc = lat_key(c, k, K_CPU), chm = lat_key(c, k, K_MEM);
-        int glo = 0, ghi = 0;
-        if (gpu) {
-            const int gm = c.gmin()[k];
-            rest_min -= gm;
-            const i64 gmax = GN - used - rest_min;
-            if (gmax < gm) {
-                st = RTGPU_UNSCHEDULABLE;
-                break;
+    for (S.k = 0; S.k < c.n; S.k++) {
+        if (S.k > 0) lat_view(tm, c, S.k - 1); /* counts of tasks before k are final */
+        {
+            const int k = S.k;
+            const int inf = c.info()[k];
+            const bool gpu = li_gpu(inf);
+            S.glo = S.ghi = 0;
+            if (gpu) {
+                const int gm = c.gmin()[k];
+                S.rest_min -= gm;
+                const i64 gmax = c.GN - S.used - S.rest_min;
+                if (gmax < gm) {
+                    S.st = RTGPU_UNSCHEDULABLE;
+                    break;
+                }
+                S.glo = gm;
+                S.ghi = (int)gmax;
             }
-            glo = gm;
-            ghi = (int)gmax;
         }
         /* ---- g-independent: the longest copy's response bounds every MR.
          * First a guess verified in one evaluation: the previous task's
@@ -1061,163 +1107,197 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
          * by ~14% (hp(k) grows by one task), so the guess usually holds and
          * saves the iterations from 0.  The exact fixed point is computed
          * only if R2 fails with the looser bound. */
-        i64 mr_ub = 0, sum_mr = -1, bsum = 0;
-        LBase lbm = {0, 0, 1};
-        bool rmax_exact = true;
-        if (p > 0) {
-            i64 bmax = 0;
-#ifndef RTGPU_LAT_NO_LANESUMS /* alloc64 +4% (scripts/gpu_lat_ab.sh r2u) */
-            lat_copy_sums(tm, ml_hi, p, B, bmax, bsum);
-#else
-            #pragma unroll 1
-            for (int j = 0; j < p; j++) {
-                bmax = tmax(bmax, (i64)ml_hi[j] + B);
-                bsum += ml_hi[j] + B;
+        S.mr_ub = 0;
+        S.sum_mr = -1;
+        S.bsum = 0;
+        S.lbm = LBase{0, 0, 1};
+        S.rmax_exact = 1;
+        if (li_p(c.info()[S.k]) > 0) {
+            {
+                const int k = S.k, inf = c.info()[k], m = li_m(inf), p = li_p(inf);
+                i64 bmax = 0, bsum = 0;
+                lat_copy_sums(tm, c.segs(k) + 2 * m + p, p, c.B()[k], bmax, bsum);
+                S.bsum = bsum;
+                S.lbm = LBase{bmax, 0, 1};
             }
-#endif
-            lbm = {bmax, 0, 1};
             double r = -1.0;
 #ifndef RTGPU_LAT_NOGUESS
-            if (mg >= 1.0) { /* (after a task without memory interference there is nothing to grow) */
+            if (S.mg >= 1.0) { /* (after a task without memory interference there is nothing to grow) */
 #else
             if (false) {
 #endif
-                const double Ng = ceil(1.5 * mg) + 1.0;
-                if (!lb_over(lbm, Ng, D)) r = lfp_lat(tm, chm, lbm, Ng, D, 1);
-                rmax_exact = r < 0;
+                const double Ng = ceil(1.5 * S.mg) + 1.0;
+                const i64 D = c.D()[S.k];
+                if (!lb_over(S.lbm, Ng, D)) r = lfp_lat(tm, lat_key(c, S.k, K_MEM), S.lbm, Ng, D, 1);
+                S.rmax_exact = r < 0;
             }
             if (r < 0) {
-                r = lfp_lat(tm, chm, lbm, (mw.bi >= 0 && lb_le(mw, lbm)) ? mwN : 0.0, D);
+                RT_COUNT(g_cnt_flfp[0]);
+                const LBase lbm = S.lbm;
+                r = lfp_lat(tm, lat_key(c, S.k, K_MEM), lbm, (S.mw.bi >= 0 && lb_le(S.mw, lbm)) ? S.mwN : 0.0,
+                            c.D()[S.k]);
                 if (r == -2.0) return ST_ESCALATE;
                 if (r < 0) {
-                    st = RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None at every count */
+                    S.st = RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None at every count */
                     break;
                 }
-                mw = lbm;
-                mwN = r;
+                S.mw = S.lbm;
+                S.mwN = r;
             }
-            mg = r;
-            mr_ub = (i64)p * (i64)r + bsum;
+            S.mg = r;
+            S.mr_ub = (i64)li_p(c.info()[S.k]) * (i64)r + S.bsum;
         } else {
-            sum_mr = 0;
+            S.sum_mr = 0;
         }
-        i64 sum_cr = -3; /* not computed yet; -1: some CR is None */
+        S.sum_cr = -3; /* not computed yet; -1: some CR is None */
         /* task k passes at count g?  1 / 0, -1 = escalate */
         auto passes = [&](int g) -> int {
-            const LBase gr = lat_grup(c, k, g);
+            RT_COUNT(g_cnt_passes);
             /* R2 (analysis.py:214) with the upper bound on sum MR (passing is
              * then exact), then with the exact sum: one CPU fixed-point site */
             #pragma unroll 1
-            for (int pass = 0; pass < 2; pass++) {
+            for (S.pass = 0; S.pass < 2; S.pass++) {
                 i64 smr = 0;
-                if (pass == 0) {
-                    smr = p > 0 ? mr_ub : 0;
+                if (S.pass == 0) {
+                    smr = li_p(c.info()[S.k]) > 0 ? S.mr_ub : 0;
                 } else {
+                    const int p = li_p(c.info()[S.k]);
                     if (p == 0) break;
-                    if (!rmax_exact) {
+                    if (!S.rmax_exact) {
                         /* the verified guess was too loose for R2: the exact
                          * fixed point of the longest copy, then R2 again */
-                        const double r = lfp_lat(tm, chm, lbm, 0.0, D);
+                        RT_COUNT(g_cnt_flfp[1]);
+                        const double r = lfp_lat(tm, lat_key(c, S.k, K_MEM), S.lbm, 0.0, c.D()[S.k]);
                         if (r < 0) return -1; /* cannot be None below a verified bound */
-                        rmax_exact = true;
-                        mw = lbm;
-                        mwN = r;
-                        mg = r;
-                        const i64 ub = (i64)p * (i64)r + bsum;
-                        if (ub < mr_ub) {
-                            mr_ub = ub;
-                            pass = -1; /* retry R2 with the exact bound */
+                        S.rmax_exact = 1;
+                        S.mw = S.lbm;
+                        S.mwN = r;
+                        S.mg = r;
+                        const i64 ub = (i64)li_p(c.info()[S.k]) * (i64)r + S.bsum;
+                        if (ub < S.mr_ub) {
+                            S.mr_ub = ub;
+                            S.pass = -1; /* retry R2 with the exact bound */
                             continue;
                         }
                     }
-                    if (sum_mr < 0) {
-                        tm.pfor(p, [&](int j) { c.bases()[j] = ml_hi[j] + B; });
-                        sum_mr = lat_chain_sum(tm, c, chm, p, D);
-                        if (sum_mr < 0) return -1; /* -2, or None (impossible: the longest copy's is not) */
+                    if (S.sum_mr < 0) {
+                        {
+                            const int k = S.k, inf = c.info()[k], m = li_m(inf), pp = li_p(inf);
+                            const Seg32 ml_hi = c.segs(k) + 2 * m + pp;
+                            const i64 B = c.B()[k];
+                            tm.pfor(pp, [&](int j) { c.bases()[j] = ml_hi[j] + B; });
+                        }
+                        RT_COUNT(g_cnt_flfp[2]);
+                        S.sum_mr = lat_chain_sum(tm, c, lat_key(c, S.k, K_MEM), li_p(c.info()[S.k]), c.D()[S.k]);
+                        if (S.sum_mr < 0) return -1; /* -2, or None (impossible: the longest copy's is not) */
                     }
-                    if (sum_mr == mr_ub) break;
-                    smr = sum_mr;
+                    if (S.sum_mr == S.mr_ub) break;
+                    smr = S.sum_mr;
                 }
-                const LBase b = {gr.bi + smr + sClu, gr.bf, gr.d};
+                const LBase gr = lat_grup(c, S.k, g);
+                const i64 D = c.D()[S.k];
+                const LBase b = {gr.bi + smr + c.sClu()[S.k], gr.bf, gr.d};
                 /* R2 passes iff lfp <= D; a pre-fixed point at the deadline
                  * itself (f(D) <= D) proves it in one evaluation -- the
                  * common case with slack; otherwise the fixed point */
                 const double nd = (double)(D - b.bi - (b.bf > 0 ? 1 : 0));
 #ifndef RTGPU_LAT_NODCHECK
-                if (nd >= 0 && lfp_lat(tm, chc, b, nd, D, 1) >= 0) return 1;
+                if (nd >= 0 && lfp_lat(tm, lat_key(c, S.k, K_CPU), b, nd, D, 1) >= 0) return 1;
 #else
                 (void)nd;
 #endif
-                const double r = lfp_lat(tm, chc, b, (cw.bi >= 0 && lb_le(cw, b)) ? cwN : 0.0, D);
-                if (r == -2.0) return -1;
-                if (r >= 0) {
-                    cw = b;
-                    cwN = r;
-                    return 1;
+                {
+                    const i64 D2 = c.D()[S.k];
+                    const LBase gr2 = lat_grup(c, S.k, g);
+                    const LBase b2 = {gr2.bi + smr + c.sClu()[S.k], gr2.bf, gr2.d};
+                    RT_COUNT(g_cnt_lfp[1]);
+                    const double r = lfp_lat(tm, lat_key(c, S.k, K_CPU), b2, (S.cw.bi >= 0 && lb_le(S.cw, b2)) ? S.cwN : 0.0, D2);
+                    if (r == -2.0) return -1;
+                    if (r >= 0) {
+                        S.cw = b2;
+                        S.cwN = r;
+                        return 1;
+                    }
                 }
             }
             /* R1 = GR up + sum MR + sum CR (analysis.py:207); CRs do not depend on g */
-            if (sum_cr == -3) {
-                tm.pfor(m, [&](int j) { c.bases()[j] = cl_hi[j]; });
-                sum_cr = lat_chain_sum(tm, c, chc, m, D);
-                if (sum_cr == -2) return -1;
+            if (S.sum_cr == -3) {
+                {
+                    const int k = S.k, inf = c.info()[k], m = li_m(inf);
+                    const Seg32 cl_hi = c.segs(k) + m;
+                    tm.pfor(m, [&](int j) { c.bases()[j] = cl_hi[j]; });
+                }
+                RT_COUNT(g_cnt_flfp[3]);
+                S.sum_cr = lat_chain_sum(tm, c, lat_key(c, S.k, K_CPU), li_m(c.info()[S.k]), c.D()[S.k]);
+                if (S.sum_cr == -2) return -1;
             }
-            if (sum_cr < 0) return 0;
-            return lb_over(LBase{gr.bi + sum_mr + sum_cr, gr.bf, gr.d}, 0.0, D) ? 0 : 1;
+            if (S.sum_cr < 0) return 0;
+            const LBase gr = lat_grup(c, S.k, g);
+            return lb_over(LBase{gr.bi + S.sum_mr + S.sum_cr, gr.bf, gr.d}, 0.0, c.D()[S.k]) ? 0 : 1;
         };
-        evals++;
+        S.evals++;
         /* smallest passing count: glo, else ghi, else bisection (own-count
          * monotone); one call site keeps one inlined copy of `passes` */
-        int g = 0, lo = glo, hi = ghi, phase = gpu ? 0 : 3;
-        int cand = gpu ? glo : 0;
-        bool fail = false;
+        {
+            const bool gpu = li_gpu(c.info()[S.k]);
+            S.g = 0;
+            S.lo = S.glo;
+            S.hi = S.ghi;
+            S.phase = gpu ? 0 : 3;
+            S.cand = gpu ? S.glo : 0;
+            S.fail = 0;
+        }
         #pragma unroll 1
         for (;;) {
-            const int o = passes(cand);
+            const int o = passes(S.cand);
             if (o < 0) return ST_ESCALATE;
+            const int phase = S.phase;
             if (phase == 3) {
-                fail = !o;
+                S.fail = !o;
                 break;
             }
             if (phase == 0) {
                 if (o) {
-                    g = glo;
+                    S.g = S.glo;
                     break;
                 }
-                if (glo >= ghi) {
-                    fail = true;
+                if (S.glo >= S.ghi) {
+                    S.fail = 1;
                     break;
                 }
-                phase = 1;
-                cand = ghi;
+                S.phase = 1;
+                S.cand = S.ghi;
                 continue;
             }
             if (phase == 1) {
                 if (!o) {
-                    fail = true;
+                    S.fail = 1;
                     break;
                 }
-                phase = 2;
+                S.phase = 2;
             } else if (o) {
-                hi = cand;
+                S.hi = S.cand;
             } else {
-                lo = cand;
+                S.lo = S.cand;
             }
+            const int lo = S.lo, hi = S.hi;
             if (hi - lo <= 1) {
-                g = hi;
+                S.g = hi;
                 break;
             }
-            cand = lo + (hi - lo) / 2;
+            S.cand = lo + (hi - lo) / 2;
         }
-        if (fail) {
-            st = RTGPU_UNSCHEDULABLE;
+        if (S.fail) {
+            S.st = RTGPU_UNSCHEDULABLE;
             break;
         }
-        if (!gpu) continue;
-        if (tm.leader()) c.g()[k] = g;
+        if (!li_gpu(c.info()[S.k])) continue;
+        if (tm.leader()) c.g()[S.k] = S.g;
         tm.sync();
-        used += g;
+        S.used += S.g;
     }
+    const int st = S.st;
+    evals = S.evals;
     if (st == RTGPU_SCHEDULABLE) tm.pfor(n, [&](int i) { vsm[i] = li_gpu(c.info()[i]) ? 2 * c.g()[i] : 0; });
     if (!bounds) return st;
     int have = n - 1;

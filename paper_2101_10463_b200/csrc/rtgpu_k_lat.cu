@@ -26,12 +26,18 @@ __global__ void __launch_bounds__(RTGPU_LAT_THREADS, MINB) lattice_kernel(KParam
     LTeam<W> tm{lane, warp % W, team + 1};
     LCtx c;
     c.hbase = nullptr;
-    c.base = team * slab_bytes;
-    c.L.init(p.dims);
+    c.sto = LSLAB_HDR + warp * LST_BYTES;
+    c.base = LSLAB_HDR + (RTGPU_LAT_THREADS / 32) * LST_BYTES + team * slab_bytes;
+    if (threadIdx.x == 0) {
+        LSlab L;
+        L.init(p.dims);
+        *(LSlab *)rt_dyn_smem = L;
+    }
+    __syncthreads();
     const bool bounds = (p.flags & RTGPU_F_BOUNDS) != 0;
     const i64 count = LIST ? (i64)p.ctr[4] : p.n_sets;
     unsigned long long *wctr = LIST ? p.lat_ctr : p.wctr0;
-    i64 *slot = (i64 *)(rt_dyn_smem + c.base + c.L.o_red) + 16; /* the team's set index */
+    i64 *slot = (i64 *)(rt_dyn_smem + c.base + c.L().o_red) + 16; /* the team's set index */
     for (;;) {
         if (tm.leader()) *slot = (i64)atomicAdd(wctr, 1ull);
         tm.sync();
@@ -105,7 +111,7 @@ static int lat_launch(const KParams &p, bool list, cudaStream_t st) {
     const LatShape sh = lat_shape(L);
     const int W = sh.W;
     const int teams = RTGPU_LAT_THREADS / 32 / W;
-    const int bytes = L.bytes * teams;
+    const int bytes = LSLAB_HDR + (RTGPU_LAT_THREADS / 32) * LST_BYTES + L.bytes * teams;
     if (bytes > 227 * 1024) {
         set_err_msg("task sets too large for shared memory");
         return -3;

@@ -24,8 +24,10 @@ long long g_cnt_flfp[8], g_cnt_fit[8], g_cnt_frounds, g_cnt_passes;
 extern "C" void host_counters(long long *out, int reset) {
     using namespace rtgpu;
     long long v[] = {g_cnt_interf[0], g_cnt_interf[1], g_cnt_lfp[0], g_cnt_lfp[1], g_cnt_eval, g_cnt_rounds,
-                     g_cnt_flfp[0], g_cnt_flfp[1], g_cnt_fit[0], g_cnt_fit[1], g_cnt_frounds, g_cnt_passes};
-    for (int i = 0; i < 12; i++) out[i] = v[i];
+                     g_cnt_flfp[0], g_cnt_flfp[1], g_cnt_fit[0], g_cnt_fit[1], g_cnt_frounds, g_cnt_passes,
+                     g_cnt_flfp[4], g_cnt_flfp[5], g_cnt_flfp[6], g_cnt_flfp[7],
+                     g_cnt_fit[4], g_cnt_fit[5], g_cnt_fit[6], g_cnt_fit[7], g_cnt_flfp[2], g_cnt_flfp[3]};
+    for (int i = 0; i < 22; i++) out[i] = v[i];
     if (reset) {
         g_cnt_interf[0] = g_cnt_interf[1] = g_cnt_lfp[0] = g_cnt_lfp[1] = g_cnt_eval = g_cnt_rounds = 0;
         for (int i = 0; i < 8; i++) g_cnt_flfp[i] = g_cnt_fit[i] = 0;
@@ -210,10 +212,12 @@ extern "C" int host_lattice_batch(const int64_t *blobs, const int64_t *set_off, 
         if (h[6] > d.MP) d.MP = (int)h[6];
     }
     LCtx c;
-    c.L.init(d);
-    std::vector<unsigned char> slab((size_t)c.L.bytes + 64);
+    c.Lh.init(d);
+    std::vector<unsigned char> slab((size_t)c.Lh.bytes + 64);
     c.hbase = (unsigned char *)(((uintptr_t)slab.data() + 15) & ~(uintptr_t)15);
     c.base = 0;
+    LSt st;
+    c.sth = &st;
     for (int64_t s = 0; s < n_sets; s++) {
         c.blob = (const i64 *)blobs + set_off[s];
         LSeq tm;
