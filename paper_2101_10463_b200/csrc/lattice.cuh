@@ -590,7 +590,7 @@ RT_HD double lfp_lat_body(const TM &tm, const LKey key, const LBase b, double N,
     c.Lh.init(Dims{key.maxn, key.MC, key.MP});
 #endif
     const LChains ch = lat_chains(c, key.task, key.res, tm.width());
-    RT_COUNT(g_cnt_flfp[4 + ch.res + 2 * mode]);
+    RT_COUNT(g_cnt_flfp[4 + ch.res + 2 * (mode ? 1 : 0)]);
     if (lb_over(b, N, D)) return -1.0;
     const double invd = b.bf ? lat_rcp(b.d) : 0.0;
     typename TM::Cache cache;
@@ -605,6 +605,12 @@ RT_HD double lfp_lat_body(const TM &tm, const LKey key, const LBase b, double N,
         const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd, tm.cache_ptr(cache), false);
         const double ub = floor(a.q + a.f + 1e-6);
         return (a.q + a.f + 1e-6 <= N) ? ub : -1.0;
+    }
+    if (mode == 2) {
+        /* an upper bound of I(b + N) (one evaluation, FP64 error < 1e-6) */
+        RT_COUNT(g_cnt_fit[6 + ch.res]);
+        const LatAcc a = lat_interf(tm, ch, (double)b.bi + N, b.bf, b.d, invd, tm.cache_ptr(cache), false);
+        return a.q + a.f + 1e-6;
     }
     #pragma unroll 1
     for (int it = 0; it < ITER_CAP; it++) {
@@ -1107,6 +1113,43 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
          * by ~14% (hp(k) grows by one task), so the guess usually holds and
          * saves the iterations from 0.  The exact fixed point is computed
          * only if R2 fails with the looser bound. */
+#ifndef RTGPU_LAT_NOQUICK
+        /* ---- quick pass at the minimum count (sufficient, one CPU and one
+         * memory evaluation): I_cpu(D) bounds the CPU interference of any
+         * window <= D, so R2 passes at glo as soon as
+         *   GR_bi + [GR_bf > 0] + sum MR + sClu + I_cpu(D) <= D
+         * (a pre-fixed point at b + floor offset <= D, analysis.py:214).
+         * That leaves room M for sum MR <= p r + bsum, r the longest copy's
+         * offset bound; r* = floor((M - bsum) / p) is verified as a memory
+         * pre-fixed point (then every MR exists and MR_j <= b_j + r*,
+         * analysis.py:156).  Otherwise the exact search below. */
+        if (li_gpu(c.info()[S.k]) && li_p(c.info()[S.k]) > 0) {
+            const int k = S.k, inf = c.info()[k], m = li_m(inf), p = li_p(inf);
+            i64 bmax = 0, bsum = 0;
+            lat_copy_sums(tm, c.segs(k) + 2 * m + p, p, c.B()[k], bmax, bsum);
+            S.bsum = bsum;
+            S.lbm = LBase{bmax, 0, 1};
+            const double iu = lfp_lat(tm, lat_key(c, S.k, K_CPU), LBase{0, 0, 1}, (double)c.D()[S.k], c.D()[S.k], 2);
+            const int kk = S.k;
+            const LBase gr = lat_grup(c, kk, S.glo);
+            const double M = (double)c.D()[kk] - iu - (double)c.sClu()[kk] - (double)gr.bi - (gr.bf > 0 ? 1.0 : 0.0) -
+                             (double)S.bsum;
+            /* (any smaller offset bound leaves R2 passing: at most the deadline) */
+            const double rs = tmin(floor(M / (double)li_p(c.info()[kk])), (double)(c.D()[kk] - S.lbm.bi));
+            if (rs >= 0) {
+                const double r = lfp_lat(tm, lat_key(c, S.k, K_MEM), S.lbm, rs, c.D()[S.k], 1);
+                if (r >= 0) {
+                    RT_COUNT(g_cnt_flfp[2]);
+                    S.mg = r;
+                    S.evals++;
+                    if (tm.leader()) c.g()[S.k] = S.glo;
+                    tm.sync();
+                    S.used += S.glo;
+                    continue;
+                }
+            }
+        }
+#endif
         S.mr_ub = 0;
         S.sum_mr = -1;
         S.bsum = 0;
@@ -1126,7 +1169,19 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
 #else
             if (false) {
 #endif
-                const double Ng = ceil(1.5 * S.mg) + 1.0;
+#ifndef RTGPU_LAT_GUESS_F
+#define RTGPU_LAT_GUESS_F 1.5
+#endif
+#ifndef RTGPU_LAT_GUESS_MODE
+#define RTGPU_LAT_GUESS_MODE 0
+#endif
+#if RTGPU_LAT_GUESS_MODE == 1
+                /* the interference grows with the hp count: k / (k - 1) */
+                const int nh = c.hpn()[S.k], ph = S.k > 0 ? c.hpn()[S.k - 1] : 0;
+                const double Ng = ceil(RTGPU_LAT_GUESS_F * S.mg * (double)nh / (double)(ph > 0 ? ph : 1)) + 1.0;
+#else
+                const double Ng = ceil(RTGPU_LAT_GUESS_F * S.mg) + 1.0;
+#endif
                 const i64 D = c.D()[S.k];
                 if (!lb_over(S.lbm, Ng, D)) r = lfp_lat(tm, lat_key(c, S.k, K_MEM), S.lbm, Ng, D, 1);
                 S.rmax_exact = r < 0;

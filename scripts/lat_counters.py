@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 from harness import harness  # noqa: E402
 
 LIB = "/tmp/libenginehost_cnt.so"
-subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-DRT_COUNTERS", *sys.argv[3:4], "-o", LIB,
+subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-DRT_COUNTERS", *(sys.argv[3].split() if len(sys.argv) > 3 else []), "-o", LIB,
                 harness.SRC], check=True)
 harness._lib = None
 harness.LIB = LIB
@@ -27,19 +27,23 @@ lib.host_counters.argtypes = [ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 
 name = sys.argv[1] if len(sys.argv) > 1 else "sweep16x9"
 per = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-n, ms = {"sweep16x9": (16, range(2, 10)), "alloc64": (64, [5])}[name]
+n, ms, gn, den = {"sweep16x9": (16, range(2, 10), 148, 20), "alloc64": (64, [5], 148, 20),
+                  "sweep8x5": (8, [5], 10, 10)}[name]
 parts = []
 for m in ms:
     for k in range(1, 11):
-        u = Fraction(k, 20)
-        gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), u, 0, 148,
+        u = Fraction(k, den)
+        gp = _native.gen_params_c(n, m, (1000, 20000), (1000, 20000), (250, 5000), u, 0, gn,
                                   Fraction(12, 100), Fraction(1), compact=True)
         parts.append(_native.generate(gp, [f"1000:{u}:{i}" for i in range(per)]))
 b, so, tb = concat_batches(parts)
 S = len(so) - 1
 cnt = (ctypes.c_longlong * 22)()
 lib.host_counters(cnt, 1)
-out = harness.lattice_batch(b, so, tb)
+if name == "sweep8x5":  # the fast path (fast_verdict), as the fast kernel runs it
+    out = harness.analyze_batch(b, so, tb, flags=0, detail=False)
+else:
+    out = harness.lattice_batch(b, so, tb)
 lib.host_counters(cnt, 0)
 v = list(cnt)
 names = ["interf0", "interf1", "lfp0", "R2_full_lfp", "eval", "rounds", "site_guessfail", "site_rmaxexact", "fit0", "fit1",
