@@ -1922,6 +1922,7 @@ RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kin
         tm.acc_sum(lg, acc, I, err);
         if (err) return (V)-1;
         V nxt = base + I;
+        if (check == 2) return I; /* the interference at `start` */
         if (check) return nxt <= r ? nxt : (V)-3;
         if (nxt <= r) return r;
         nxt += tm.acc_rho(acc);
@@ -2045,202 +2046,249 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
             glo = t.gmin;
             ghi = (int)gmax;
         }
-        /* ---- g-independent part: memory responses (Lemma 6) */
-        V sum_mr = 0, mr_ub = 0;
-        bool have_exact_mr = t.p == 0, rmax_exact = true;
-        i64 bsum_k = 0;
-        V bmax_k = 0;
-        if (t.p > 0) {
-            i64 bmax_t = 0, bsum_t = 0;
-#if defined(__CUDA_ARCH__) && !defined(RTGPU_FAST_NO_LANESUMS)
-            { /* one load per lane and two butterflies (p <= 30): +1.1% on the
-               * 8 x 5 sweep over the sequential loop (scripts/gpu_lat_ab.sh r2u) */
-                const i64 v = tm.lane < t.p ? ml_hi[tm.lane] + t.B : 0;
-                bmax_t = v;
-                bsum_t = v;
-                #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    bmax_t = tmax(bmax_t, shfl_x(bmax_t, off));
-                    bsum_t += shfl_x(bsum_t, off);
+        int g = glo;
+        bool quick = false;
+#ifndef RTGPU_FAST_NOQUICK
+        /* ---- quick pass at the minimum count (sufficient; two evaluations):
+         * R2 (analysis.py:214) passes at glo if its base plus I_cpu(D) fits
+         * D (f(D) <= D); that leaves room M for sum MR <= p r + bsum (r the
+         * longest copy's offset, MR_j <= b_j + r by lfp(b') >= lfp(b) +
+         * (b' - b)), and r* = floor(M / p) is verified as a memory
+         * pre-fixed point (then every MR exists, analysis.py:156).  Any
+         * failure falls through to the exact search below. */
+        if (t.isgpu && t.p > 0) {
+            const V iu = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, (V)0, D, D, 2);
+            if (iu >= 0) {
+                i64 bmax_t = 0, bsum_t = 0;
+#if defined(__CUDA_ARCH__)
+                {
+                    const i64 v = tm.lane < t.p ? ml_hi[tm.lane] + t.B : 0;
+                    bmax_t = v;
+                    bsum_t = v;
+                    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        bmax_t = tmax(bmax_t, shfl_x(bmax_t, off));
+                        bsum_t += shfl_x(bsum_t, off);
+                    }
+                }
+#else
+                for (int j = 0; j < t.p; j++) {
+                    bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
+                    bsum_t += ml_hi[j] + t.B;
+                }
+#endif
+                const V grup = (V)t.sInfl * (lg_tab ? outs[glo - 1] : (V)(q / (2 * A * (Qt)glo))) +
+                               Num<V>::sc(t.sGL, q);
+                const V M = D - iu - Num<V>::sc(t.sClu, q) - grup - Num<V>::sc(bsum_t, q);
+                if (M >= 0) {
+                    const V bmax = Num<V>::sc(bmax_t, q);
+                    V rs = Num<V>::floordiv(M, (V)t.p);
+                    if (rs > D - bmax) rs = D - bmax;
+                    if (rs >= 0 && lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, bmax + rs, D, 1) >= 0)
+                        quick = true;
                 }
             }
-#else
-            #pragma unroll 1
-            for (int j = 0; j < t.p; j++) {
-                bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
-                bsum_t += ml_hi[j] + t.B;
-            }
-#endif
-            const V bmax = Num<V>::sc(bmax_t, q);
-            bsum_k = bsum_t;
-            bmax_k = bmax;
-            /* warm start across tasks: hp(k) grows with k, so the memory
-             * interference of task k is pointwise >= that of any earlier
-             * task, and lfp(b') >= lfp(b) + (b' - b) for b' >= b: the
-             * previous task's fixed point shifted by the base difference is
-             * below this one */
-            V rmax = -1;
-            /* off by default: on the 8 x 5 benchmark the longer code costs more
-             * than the saved iterations (scripts/gpu_lat_ab.sh r2l: 24.4 vs
-             * 25.5 M sets/s); the lattice path keeps it (alloc64 +14%) */
-#ifdef RTGPU_FAST_GUESS
-            if (mem_guess > 0) {
-#else
-            if (false) {
-#endif
-                /* the previous task's memory offset grown by half, verified
-                 * as a pre-fixed point in one evaluation (then the lfp is at
-                 * most f(U) <= D: every MR exists, bounded via f(U)); the
-                 * exact fixed point only if R2 needs it (lattice.cuh) */
-                const V U = bmax + Num<V>::sc(1, q) + floor(mem_guess * 1.5);
-                if (U <= D) rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, U, D, 1);
-                rmax_exact = rmax < 0;
-            }
-            if (rmax < 0) {
-                V start = bmax;
-                if (mem_prev_b >= 0 && bmax >= mem_prev_b) start = tmax(bmax, mem_prev_r + (bmax - mem_prev_b));
-                rmax = start > D ? (V)-1 : lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, start, D);
-                if (rmax == (V)-2) return ST_ESCALATE;
-                if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
-                mem_prev_b = bmax;
-                mem_prev_r = rmax;
-            }
-            mem_guess = rmax - bmax;
-            mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
         }
-        V sum_cr = -1; /* not computed yet; -2: some CR is None */
-        /* task k passes at count g?  (R2 with the MR upper bound, then exact) */
-        auto passes = [&](int g) -> int {
-            RT_COUNT(g_cnt_passes);
-            const V grup = t.isgpu ? (V)t.sInfl * (lg_tab ? outs[g - 1] : (V)(q / (2 * A * (Qt)g))) +
-                                         Num<V>::sc(t.sGL, q)
-                                   : (V)0;
-            const V cl = Num<V>::sc(t.sClu, q);
-            if (t.p > 0 || !have_exact_mr) {
-                V b2 = grup + mr_ub + cl;
-                /* R2 proven at the deadline itself (f(D) <= D) in one evaluation */
-                if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
-                    return 1;
-                if (!rmax_exact) {
-                    /* the verified memory bound was loose: the exact one */
-                    const V rm = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax_k, bmax_k, D);
-                    if (rm < 0) return -1; /* cannot be None below a verified bound */
-                    rmax_exact = true;
-                    mem_prev_b = bmax_k;
-                    mem_prev_r = rm;
-                    mem_guess = rm - bmax_k;
-                    mr_ub = (V)t.p * (rm - bmax_k) + Num<V>::sc(bsum_k, q);
-                    b2 = grup + mr_ub + cl;
+#endif
+        if (!quick) {
+            /* ---- g-independent part: memory responses (Lemma 6) */
+            V sum_mr = 0, mr_ub = 0;
+            bool have_exact_mr = t.p == 0, rmax_exact = true;
+            i64 bsum_k = 0;
+            V bmax_k = 0;
+            if (t.p > 0) {
+                i64 bmax_t = 0, bsum_t = 0;
+    #if defined(__CUDA_ARCH__) && !defined(RTGPU_FAST_NO_LANESUMS)
+                { /* one load per lane and two butterflies (p <= 30): +1.1% on the
+                   * 8 x 5 sweep over the sequential loop (scripts/gpu_lat_ab.sh r2u) */
+                    const i64 v = tm.lane < t.p ? ml_hi[tm.lane] + t.B : 0;
+                    bmax_t = v;
+                    bsum_t = v;
+                    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        bmax_t = tmax(bmax_t, shfl_x(bmax_t, off));
+                        bsum_t += shfl_x(bsum_t, off);
+                    }
+                }
+    #else
+                #pragma unroll 1
+                for (int j = 0; j < t.p; j++) {
+                    bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
+                    bsum_t += ml_hi[j] + t.B;
+                }
+    #endif
+                const V bmax = Num<V>::sc(bmax_t, q);
+                bsum_k = bsum_t;
+                bmax_k = bmax;
+                /* warm start across tasks: hp(k) grows with k, so the memory
+                 * interference of task k is pointwise >= that of any earlier
+                 * task, and lfp(b') >= lfp(b) + (b' - b) for b' >= b: the
+                 * previous task's fixed point shifted by the base difference is
+                 * below this one */
+                V rmax = -1;
+                /* off by default: on the 8 x 5 benchmark the longer code costs more
+                 * than the saved iterations (scripts/gpu_lat_ab.sh r2l: 24.4 vs
+                 * 25.5 M sets/s); the lattice path keeps it (alloc64 +14%) */
+    #ifdef RTGPU_FAST_GUESS
+                if (mem_guess > 0) {
+    #else
+                if (false) {
+    #endif
+                    /* the previous task's memory offset grown by half, verified
+                     * as a pre-fixed point in one evaluation (then the lfp is at
+                     * most f(U) <= D: every MR exists, bounded via f(U)); the
+                     * exact fixed point only if R2 needs it (lattice.cuh) */
+                    const V U = bmax + Num<V>::sc(1, q) + floor(mem_guess * 1.5);
+                    if (U <= D) rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, U, D, 1);
+                    rmax_exact = rmax < 0;
+                }
+                if (rmax < 0) {
+                    V start = bmax;
+                    if (mem_prev_b >= 0 && bmax >= mem_prev_b) start = tmax(bmax, mem_prev_r + (bmax - mem_prev_b));
+                    rmax = start > D ? (V)-1 : lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, start, D);
+                    if (rmax == (V)-2) return ST_ESCALATE;
+                    if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
+                    mem_prev_b = bmax;
+                    mem_prev_r = rmax;
+                }
+                mem_guess = rmax - bmax;
+                mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
+            }
+            V sum_cr = -1; /* not computed yet; -2: some CR is None */
+            /* task k passes at count g?  (R2 with the MR upper bound, then exact) */
+            auto passes = [&](int g) -> int {
+                RT_COUNT(g_cnt_passes);
+                const V grup = t.isgpu ? (V)t.sInfl * (lg_tab ? outs[g - 1] : (V)(q / (2 * A * (Qt)g))) +
+                                             Num<V>::sc(t.sGL, q)
+                                       : (V)0;
+                const V cl = Num<V>::sc(t.sClu, q);
+                if (t.p > 0 || !have_exact_mr) {
+                    V b2 = grup + mr_ub + cl;
+                    /* R2 proven at the deadline itself (f(D) <= D) in one evaluation */
                     if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
                         return 1;
+                    if (!rmax_exact) {
+                        /* the verified memory bound was loose: the exact one */
+                        const V rm = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax_k, bmax_k, D);
+                        if (rm < 0) return -1; /* cannot be None below a verified bound */
+                        rmax_exact = true;
+                        mem_prev_b = bmax_k;
+                        mem_prev_r = rm;
+                        mem_guess = rm - bmax_k;
+                        mr_ub = (V)t.p * (rm - bmax_k) + Num<V>::sc(bsum_k, q);
+                        b2 = grup + mr_ub + cl;
+                        if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
+                            return 1;
+                    }
+                    const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
+                    if (r == (V)-2) return -1;
+                    if (r >= 0) return 1;
+                    if (!have_exact_mr) {
+                        /* exact memory responses, ascending bases with warm starts */
+                        tm.pfor(t.p, [&](int j) { bases[j] = Num<V>::sc(ml_hi[j] + t.B, q); });
+                        tm.pfor(t.p, [&](int j) {
+                            int rk = 0;
+                            #pragma unroll 1
+                            for (int x = 0; x < t.p; x++)
+                                rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
+                            ord[rk] = j;
+                        });
+                        V pb = 0, pr = 0, acc = 0;
+                        #pragma unroll 1
+                        for (int st = 0; st < t.p; st++) {
+                            const V b = bases[ord[st]];
+                            const V r0 = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, b,
+                                                  st ? tmax(b, pr + (b - pb)) : b, D);
+                            if (r0 < 0) return r0 == (V)-2 ? -1 : 0; /* cannot be None: rmax was not */
+                            acc += r0;
+                            pb = b;
+                            pr = r0;
+                        }
+                        sum_mr = acc;
+                        have_exact_mr = true;
+                    }
+                    if (sum_mr != mr_ub) {
+                        const V b3 = grup + sum_mr + cl;
+                        const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
+                        if (r3 == (V)-2) return -1;
+                        if (r3 >= 0) return 1;
+                    }
+                } else {
+                    const V b3 = grup + cl;
+                    if (RTGPU_FAST_DCHECK && b3 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, D, D, 1) >= 0)
+                        return 1;
+                    const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
+                    if (r3 == (V)-2) return -1;
+                    if (r3 >= 0) return 1;
                 }
-                const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
-                if (r == (V)-2) return -1;
-                if (r >= 0) return 1;
-                if (!have_exact_mr) {
-                    /* exact memory responses, ascending bases with warm starts */
-                    tm.pfor(t.p, [&](int j) { bases[j] = Num<V>::sc(ml_hi[j] + t.B, q); });
-                    tm.pfor(t.p, [&](int j) {
+                /* R1 = GR up + sum MR + sum CR (analysis.py:207) */
+                if (sum_cr == -1) {
+                    tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q); });
+                    tm.pfor(t.m, [&](int j) {
                         int rk = 0;
                         #pragma unroll 1
-                        for (int x = 0; x < t.p; x++)
+                        for (int x = 0; x < t.m; x++)
                             rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
                         ord[rk] = j;
                     });
                     V pb = 0, pr = 0, acc = 0;
                     #pragma unroll 1
-                    for (int st = 0; st < t.p; st++) {
+                    for (int st = 0; st < t.m; st++) {
                         const V b = bases[ord[st]];
-                        const V r0 = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, b,
+                        const V r0 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b,
                                               st ? tmax(b, pr + (b - pb)) : b, D);
-                        if (r0 < 0) return r0 == (V)-2 ? -1 : 0; /* cannot be None: rmax was not */
+                        if (r0 == (V)-2) return -1;
+                        if (r0 < 0) {
+                            acc = -2;
+                            break;
+                        }
                         acc += r0;
                         pb = b;
                         pr = r0;
                     }
-                    sum_mr = acc;
-                    have_exact_mr = true;
+                    sum_cr = acc;
                 }
-                if (sum_mr != mr_ub) {
-                    const V b3 = grup + sum_mr + cl;
-                    const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
-                    if (r3 == (V)-2) return -1;
-                    if (r3 >= 0) return 1;
-                }
-            } else {
-                const V b3 = grup + cl;
-                if (RTGPU_FAST_DCHECK && b3 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, D, D, 1) >= 0)
-                    return 1;
-                const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
-                if (r3 == (V)-2) return -1;
-                if (r3 >= 0) return 1;
-            }
-            /* R1 = GR up + sum MR + sum CR (analysis.py:207) */
-            if (sum_cr == -1) {
-                tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q); });
-                tm.pfor(t.m, [&](int j) {
-                    int rk = 0;
-                    #pragma unroll 1
-                    for (int x = 0; x < t.m; x++)
-                        rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
-                    ord[rk] = j;
-                });
-                V pb = 0, pr = 0, acc = 0;
-                #pragma unroll 1
-                for (int st = 0; st < t.m; st++) {
-                    const V b = bases[ord[st]];
-                    const V r0 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b,
-                                          st ? tmax(b, pr + (b - pb)) : b, D);
-                    if (r0 == (V)-2) return -1;
-                    if (r0 < 0) {
-                        acc = -2;
-                        break;
-                    }
-                    acc += r0;
-                    pb = b;
-                    pr = r0;
-                }
-                sum_cr = acc;
-            }
-            if (sum_cr < 0) return 0;
-            return grup + sum_mr + sum_cr <= D ? 1 : 0;
-        };
-        c.evals++;
-        /* smallest passing count: glo, else ghi, else bisection -- one call
-         * site for `passes` keeps a single inlined copy */
-        int g = 0, lo = glo, hi = ghi, phase = t.isgpu ? 0 : 3;
-        int cand = t.isgpu ? glo : 0;
-        #pragma unroll 1
-        for (;;) {
-            const int o = passes(cand);
-            if (o < 0) return ST_ESCALATE;
-            if (phase == 3) { /* pure-CPU task: one evaluation */
-                if (!o) return RTGPU_UNSCHEDULABLE;
-                break;
-            }
-            if (phase == 0) {
-                if (o) {
-                    g = glo;
+                if (sum_cr < 0) return 0;
+                return grup + sum_mr + sum_cr <= D ? 1 : 0;
+            };
+            c.evals++;
+            /* smallest passing count: glo, else ghi, else bisection -- one call
+             * site for `passes` keeps a single inlined copy */
+            g = 0;
+            int lo = glo, hi = ghi, phase = t.isgpu ? 0 : 3;
+            int cand = t.isgpu ? glo : 0;
+            #pragma unroll 1
+            for (;;) {
+                const int o = passes(cand);
+                if (o < 0) return ST_ESCALATE;
+                if (phase == 3) { /* pure-CPU task: one evaluation */
+                    if (!o) return RTGPU_UNSCHEDULABLE;
                     break;
                 }
-                if (glo >= ghi) return RTGPU_UNSCHEDULABLE;
-                phase = 1;
-                cand = ghi;
-                continue;
+                if (phase == 0) {
+                    if (o) {
+                        g = glo;
+                        break;
+                    }
+                    if (glo >= ghi) return RTGPU_UNSCHEDULABLE;
+                    phase = 1;
+                    cand = ghi;
+                    continue;
+                }
+                if (phase == 1) {
+                    if (!o) return RTGPU_UNSCHEDULABLE;
+                    phase = 2;
+                } else if (o) {
+                    hi = cand;
+                } else {
+                    lo = cand;
+                }
+                if (hi - lo <= 1) {
+                    g = hi;
+                    break;
+                }
+                cand = lo + (hi - lo) / 2;
             }
-            if (phase == 1) {
-                if (!o) return RTGPU_UNSCHEDULABLE;
-                phase = 2;
-            } else if (o) {
-                hi = cand;
-            } else {
-                lo = cand;
-            }
-            if (hi - lo <= 1) {
-                g = hi;
-                break;
-            }
-            cand = lo + (hi - lo) / 2;
         }
         if (!t.isgpu) continue;
         tm.sync();
