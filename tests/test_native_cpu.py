@@ -18,6 +18,8 @@ def declared_symbols():
         text = open(h).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names |= set(re.findall(r"\b(rtgpu_\w+)\s*\(", text))
+        # header-only helpers (static inline, e.g. rtgpu_rec_word) are not exports
+        names -= set(re.findall(r"static\s+inline\s+[\w\s\*]*?\b(rtgpu_\w+)\s*\(", text))
     return names
 
 
