@@ -18,8 +18,8 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(LIB) or (
-            os.path.getmtime(LIB) < os.path.getmtime(os.path.join(HERE, "rtgpu_oracle.c"))):
+    deps = [os.path.join(HERE, "rtgpu_oracle.c"), os.path.join(os.path.dirname(HERE), "include", "rtgpu.h")]
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(d) for d in deps):
         subprocess.run(["make", "-s", "-C", HERE], check=True)
     return LIB
 

@@ -97,7 +97,7 @@ typedef struct {
 static __thread int64_t seg64[MAXT * (2 * MAXM + 2 * MAXP + 4 * MAXG)];
 
 static int parse_set(const int64_t *b, oset *s) {
-    const int compact = b[7] == 1;
+    const int compact = b[7] == 1 || b[7] == 2; /* 2: int32 task records too */
     int64_t used64 = 0;
     s->n = (int)b[0];
     s->gn = (int)b[1];
@@ -105,15 +105,14 @@ static int parse_set(const int64_t *b, oset *s) {
     s->A = b[3];
     if (s->n < 0 || s->n > MAXT || s->A < 1 || (s->mm != 0 && s->mm != 1)) return -1;
     for (int i = 0; i < s->n; i++) {
-        const int64_t *r = b + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
         otask *t = &s->t[i];
-        t->m = (int)r[0];
-        t->p = (int)r[1];
+        t->m = (int)rtgpu_rec_word(b, i, 0);
+        t->p = (int)rtgpu_rec_word(b, i, 1);
         t->g = t->m - 1;
-        t->D = r[2];
-        t->T = r[3];
-        t->prio = r[4];
-        t->seg_off = r[5];
+        t->D = rtgpu_rec_word(b, i, 2);
+        t->T = rtgpu_rec_word(b, i, 3);
+        t->prio = rtgpu_rec_word(b, i, 4);
+        t->seg_off = rtgpu_rec_word(b, i, 5);
         if (t->m < 1 || t->m > MAXM || t->p < 0 || t->p > MAXP) return -1;
         const int64_t *q = b + t->seg_off;
         if (compact) {

@@ -94,14 +94,25 @@ class TaskArrays:
             raise ValueError("from_blobs: sets of one shape (equal blob sizes) expected")
         B = blobs[int(set_off[0]):int(set_off[-1])].reshape(S, W)
         n, mm, cform = int(B[0, 0]), int(B[0, 2]), int(B[0, 7])
-        rec = B[:, HDR_WORDS:HDR_WORDS + TASK_WORDS * n].reshape(S, n, TASK_WORDS)
+        rw = TASK_WORDS // 2 if cform == 2 else TASK_WORDS  # int64 words per record (2: packed records)
+        rec = B[:, HDR_WORDS:HDR_WORDS + rw * n].reshape(S, n, rw)
+        if cform == 2:  # D, T, m | p << 8 | index << 16, priority (int32) | seg_off << 32
+            w = rec
+            rec = np.zeros((S, n, TASK_WORDS), np.int64)
+            rec[:, :, 0] = w[:, :, 2] & 0xff
+            rec[:, :, 1] = (w[:, :, 2] >> 8) & 0xff
+            rec[:, :, 2] = w[:, :, 0]
+            rec[:, :, 3] = w[:, :, 1]
+            rec[:, :, 4] = (w[:, :, 3] & 0xffffffff).astype(np.uint32).view(np.int32)
+            rec[:, :, 5] = w[:, :, 3] >> 32
+            rec[:, :, 6] = w[:, :, 2] >> 16
         m, p = int(rec[0, 0, 0]), int(rec[0, 0, 1])
         g = m - 1
         if not (np.all(B[:, 0] == n) and np.all(B[:, 2] == mm) and np.all(B[:, 7] == cform)
                 and np.all(rec[:, :, 0] == m) and np.all(rec[:, :, 1] == p)):
             raise ValueError("from_blobs: sets of one shape expected")
         per = 2 * m + 2 * p + 4 * g
-        base = HDR_WORDS + TASK_WORDS * n
+        base = HDR_WORDS + rw * n
         area = B[:, base:].copy().view(np.int32) if cform else B[:, base:]
         start = rec[:, :, 5] - (2 * base if cform else base)  # [S, n] offsets inside the area
         idx = start[:, :, None] + np.arange(per)[None, None, :]

@@ -638,7 +638,7 @@ RT_NI double lfp_lat(const TM &tm, const LKey key, const LBase b, double N, i64 
  * D + T + every sum; B[i] receives the task's longest copy.  Tasks the
  * lattice path does not take are flagged TF_UNSUP / TF_IRREG / TF_INV. */
 RT_HD i64 lat_load(const LCtx &c, int i) {
-    const i64 *r = c.blob + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
+    const RecP r = rec_at(c.blob, i);
     const int m = (int)r[0], p = (int)r[1];
     const i64 D = r[2], T = r[3];
     const int want_p = m < 2 ? 0 : (c.mm == RTGPU_TWO_COPY ? 2 * m - 2 : m - 1);
@@ -759,7 +759,7 @@ RT_HD void lat_build_chain(double *v, int PM, int q, int lane, double e_j, doubl
 }
 
 RT_HD void lat_view_lane(const LCtx &c, int i, int lane) {
-    const i64 *r = c.blob + RTGPU_HDR_WORDS + RTGPU_TASK_WORDS * i;
+    const RecP r = rec_at(c.blob, i);
     const int info = c.info()[i];
     const int m = li_m(info), p = li_p(info);
     const i64 T = r[3], D = r[2];
@@ -1017,7 +1017,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
     c.mm = (int)h[2];
     c.A = A;
     evals = 0;
-    if (h[7] != 1 || n < 1 || n > c.L().maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > (1 << 20))
+    if ((h[7] != 1 && h[7] != 2) || n < 1 || n > c.L().maxn || A < 1 || (c.mm != 0 && c.mm != 1) || GN < 1 || GN > (1 << 20))
         return ST_ESCALATE;
     /* loads; each task's range bound parks in its (not yet built) CPU view */
     tm.pfor(n, [&](int i) {
@@ -1029,7 +1029,6 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         }
     });
     const int *info = c.info();
-    const i64 *rec = h + RTGPU_HDR_WORDS;
     i64 need = 0, vb_max = 0;
     /* reference order: the first task whose minimum-count search raises or fails */
     #pragma unroll 1
@@ -1039,7 +1038,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         if (fl & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE; /* empty report */
         if (li_gpu(info[k])) need += c.gmin()[k];
         vb_max = tmax(vb_max, *(const i64 *)(c.VC() + (size_t)k * c.L().SC));
-        if (k > 0 && rec[RTGPU_TASK_WORDS * k + 4] < rec[RTGPU_TASK_WORDS * (k - 1) + 4]) return ST_ESCALATE;
+        if (k > 0 && rec_at(h, k)[4] < rec_at(h, k - 1)[4]) return ST_ESCALATE;
     }
     if (need > GN) return RTGPU_UNSCHEDULABLE; /* no allocation at all: empty report */
     int gtop = 1;
@@ -1055,14 +1054,14 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
      * task's longest copy until the barrier) */
     i64 *bases = c.bases();
     tm.pfor(n, [&](int k) {
-        const i64 pk = rec[RTGPU_TASK_WORDS * k + 4];
+        const i64 pk = rec_at(h, k)[4];
         int first = k;
-        while (first > 0 && rec[RTGPU_TASK_WORDS * (first - 1) + 4] == pk) first--;
+        while (first > 0 && rec_at(h, first - 1)[4] == pk) first--;
         c.hpn()[k] = first;
         i64 b = 0;
         #pragma unroll 1
         for (int i = k + 1; i < n; i++)
-            if (rec[RTGPU_TASK_WORDS * i + 4] > pk) b = tmax(b, c.B()[i]);
+            if (rec_at(h, i)[4] > pk) b = tmax(b, c.B()[i]);
         *(i64 *)(c.VC() + (size_t)k * c.L().SC) = b;
     });
     tm.pfor(n, [&](int k) { c.B()[k] = *(const i64 *)(c.VC() + (size_t)k * c.L().SC); });

@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(RTGPU_LAT_THREADS, MINB) lattice_kernel(KParam
         /* list stage: the sets the fast path could not take because of their
          * width (more than 64 SMs); its range escalations (a few per 10^5 on
          * 10 SMs) stay with the int64 fast path, which decides them sooner */
-        if (LIST && c.blob[1] <= 64 && c.blob[7] == 1) continue;
+        if (LIST && c.blob[1] <= 64 && c.blob[7] >= 1) continue;
         const i64 tb = p.task_base[s];
         i64 evals = 0;
         const int st = lattice_set(tm, c, bounds, p.vsm + tb, bounds ? p.e2e + tb : nullptr,

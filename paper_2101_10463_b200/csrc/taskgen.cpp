@@ -334,6 +334,7 @@ bool gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
         }
     const int seg_words = 2 * m + 2 * pm + 4 * (m - 1);
     const bool c32 = p->seg_int32 != 0;
+    const bool r32 = p->seg_int32 == 2; /* int32 task records too */
     const int64_t words = rtgpu_gen_blob_words(p);
     out[0] = n;
     out[1] = p->physical_sms;
@@ -342,24 +343,26 @@ bool gen_one(const rtgpu_gen_params *p, MT &g, int64_t *out) {
     out[4] = words;
     out[5] = m;
     out[6] = pm;
-    out[7] = c32 ? 1 : 0;
+    out[7] = r32 ? 2 : (c32 ? 1 : 0);
     /* segment areas after the records; seg_off in int64 words or int32 elements */
-    int64_t seg = (RTGPU_HDR_WORDS + (int64_t)n * RTGPU_TASK_WORDS) * (c32 ? 2 : 1);
+    int64_t seg = (RTGPU_HDR_WORDS + (int64_t)n * RTGPU_REC_WORDS(out[7])) * (c32 ? 2 : 1);
     int32_t *out32 = (int32_t *)out;
     /* tasks in priority order (TaskSet.by_priority) */
     std::vector<int> byp(n);
     for (int i = 0; i < n; i++) byp[prio[i] - 1] = i;
     for (int r = 0; r < n; r++) {
         Draft &d = dr[byp[r]];
-        int64_t *rec = out + RTGPU_HDR_WORDS + (int64_t)r * RTGPU_TASK_WORDS;
-        rec[0] = m;
-        rec[1] = pm;
-        rec[2] = d.D;
-        rec[3] = d.D;
-        rec[4] = r + 1;
-        rec[5] = seg;
-        rec[6] = d.idx;
-        rec[7] = 0;
+        const int64_t rv[RTGPU_TASK_WORDS] = {m, pm, d.D, d.D, r + 1, seg, d.idx, 0};
+        if (r32) { /* packed record (include/rtgpu.h): D, T, m | p | index, priority | seg_off */
+            int64_t *rec = out + RTGPU_HDR_WORDS + (int64_t)r * (RTGPU_TASK_WORDS / 2);
+            rec[0] = rv[2];
+            rec[1] = rv[3];
+            rec[2] = (rv[0] & 0xff) | (rv[1] & 0xff) << 8 | rv[6] << 16;
+            rec[3] = (int64_t)((uint64_t)(uint32_t)(int32_t)rv[4] | (uint64_t)rv[5] << 32);
+        } else {
+            int64_t *rec = out + RTGPU_HDR_WORDS + (int64_t)r * RTGPU_TASK_WORDS;
+            for (int f = 0; f < RTGPU_TASK_WORDS; f++) rec[f] = rv[f];
+        }
         std::vector<int64_t> v;
         v.reserve(seg_words);
         for (int j = 0; j < m; j++) v.push_back(d.cl_lo[j]);
@@ -387,7 +390,7 @@ int64_t rtgpu_gen_blob_words(const rtgpu_gen_params *p) {
     const int n = p->n_tasks, m = p->n_subtasks;
     const int pm = m < 2 ? 0 : (p->mem_model == RTGPU_ONE_COPY ? m - 1 : 2 * m - 2);
     const int64_t seg = (int64_t)n * (2 * m + 2 * pm + 4 * (m - 1));
-    return RTGPU_HDR_WORDS + (int64_t)n * RTGPU_TASK_WORDS + (p->seg_int32 ? (seg + 1) / 2 : seg);
+    return RTGPU_HDR_WORDS + (int64_t)n * RTGPU_REC_WORDS(p->seg_int32) + (p->seg_int32 ? (seg + 1) / 2 : seg);
 }
 
 int rtgpu_generate(const rtgpu_gen_params *p, int64_t n_sets, const int64_t *int_seeds,
