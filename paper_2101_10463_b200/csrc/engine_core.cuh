@@ -1965,243 +1965,6 @@ RT_NI V lfp_fast(const TM &tm, const TaskRec *tr, const V *views, int k, int kin
 /* ST_ESCALATE_RANGE: only the scale did not fit V (the int64 instance may) */
 enum { ST_ESCALATE_RANGE = 98 };
 
-/* The exact search for task k (everything after the quick pass fails):
- * out of line, so the fast kernel's hot path -- quick pass and loop control
- * -- stays compact in the instruction cache (r2zd: 30% no-instruction stalls
- * with it inlined).  Returns the count (0 for a pure-CPU task that passes),
- * -1 unschedulable, -2 escalate. */
-template <class V> struct FastTask {
-    typename Num<V>::Qt q;
-    i64 A;
-    V D, mem_prev_b, mem_prev_r, mem_guess; /* the warm starts live across tasks */
-    int k, glo, ghi, lg_tab;
-};
-
-template <class V, class TM>
-RT_NI int fast_task_exact(const TM &tm, SetCtx<V> &c, FastTask<V> &ft) {
-    typedef i64 Qt;
-    TaskRec *tr = c.TR();
-    const int k = ft.k, glo = ft.glo, ghi = ft.ghi;
-    const bool lg_tab = ft.lg_tab != 0;
-    const Qt q = ft.q;
-    const i64 A = ft.A;
-    const V D = ft.D;
-    V mem_prev_b = ft.mem_prev_b, mem_prev_r = ft.mem_prev_r, mem_guess = ft.mem_guess;
-    const int lgC = c.lgC, lgM = c.lgM, halfC = c.halfC, halfM = c.halfM;
-    const int SC = c.L.SC, SM = c.L.SM, MC = c.MC, MP = c.MP;
-    V *vc = c.VC(), *vm = c.VM();
-    V *bases = c.SCR();
-    V *outs = c.SCR() + (c.MP + c.MC + 2);
-    int *ord = (int *)(c.SCR() + c.L.scr_n) - 32;
-    const TaskRec &t = tr[k];
-    const Seg32 sg{(const int32_t *)c.blob + t.seg};
-    const Seg32 cl_hi = sg + t.m, ml_hi = sg + 2 * t.m + t.p;
-    int g = glo;
-    (void)vc, (void)vm;
-    /* ---- g-independent part: memory responses (Lemma 6) */
-    V sum_mr = 0, mr_ub = 0;
-    bool have_exact_mr = t.p == 0, rmax_exact = true;
-    i64 bsum_k = 0;
-    V bmax_k = 0;
-    if (t.p > 0) {
-        i64 bmax_t = 0, bsum_t = 0;
-#if defined(__CUDA_ARCH__) && !defined(RTGPU_FAST_NO_LANESUMS)
-        { /* one load per lane and two butterflies (p <= 30): +1.1% on the
-           * 8 x 5 sweep over the sequential loop (scripts/gpu_lat_ab.sh r2u) */
-            const i64 v = tm.lane < t.p ? ml_hi[tm.lane] + t.B : 0;
-            bmax_t = v;
-            bsum_t = v;
-            #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                bmax_t = tmax(bmax_t, shfl_x(bmax_t, off));
-                bsum_t += shfl_x(bsum_t, off);
-            }
-        }
-#else
-        #pragma unroll 1
-        for (int j = 0; j < t.p; j++) {
-            bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
-            bsum_t += ml_hi[j] + t.B;
-        }
-#endif
-        const V bmax = Num<V>::sc(bmax_t, q);
-        bsum_k = bsum_t;
-        bmax_k = bmax;
-        /* warm start across tasks: hp(k) grows with k, so the memory
-         * interference of task k is pointwise >= that of any earlier
-         * task, and lfp(b') >= lfp(b) + (b' - b) for b' >= b: the
-         * previous task's fixed point shifted by the base difference is
-         * below this one */
-        V rmax = -1;
-        /* off by default: on the 8 x 5 benchmark the longer code costs more
-         * than the saved iterations (scripts/gpu_lat_ab.sh r2l: 24.4 vs
-         * 25.5 M sets/s); the lattice path keeps it (alloc64 +14%) */
-#ifdef RTGPU_FAST_GUESS
-        if (mem_guess > 0) {
-#else
-        if (false) {
-#endif
-            /* the previous task's memory offset grown by half, verified
-             * as a pre-fixed point in one evaluation (then the lfp is at
-             * most f(U) <= D: every MR exists, bounded via f(U)); the
-             * exact fixed point only if R2 needs it (lattice.cuh) */
-            const V U = bmax + Num<V>::sc(1, q) + floor(mem_guess * 1.5);
-            if (U <= D) rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, U, D, 1);
-            rmax_exact = rmax < 0;
-        }
-        if (rmax < 0) {
-            V start = bmax;
-            if (mem_prev_b >= 0 && bmax >= mem_prev_b) start = tmax(bmax, mem_prev_r + (bmax - mem_prev_b));
-            rmax = start > D ? (V)-1 : lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, start, D);
-            if (rmax == (V)-2) return -2;
-            if (rmax < 0) return -1; /* the longest copy's MR is None */
-            mem_prev_b = bmax;
-            mem_prev_r = rmax;
-        }
-        mem_guess = rmax - bmax;
-        mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
-    }
-    V sum_cr = -1; /* not computed yet; -2: some CR is None */
-    /* task k passes at count g?  (R2 with the MR upper bound, then exact) */
-    auto passes = [&](int g) -> int {
-        RT_COUNT(g_cnt_passes);
-        const V grup = t.isgpu ? (V)t.sInfl * (lg_tab ? outs[g - 1] : (V)(q / (2 * A * (Qt)g))) +
-                                     Num<V>::sc(t.sGL, q)
-                               : (V)0;
-        const V cl = Num<V>::sc(t.sClu, q);
-        if (t.p > 0 || !have_exact_mr) {
-            V b2 = grup + mr_ub + cl;
-            /* R2 proven at the deadline itself (f(D) <= D) in one evaluation */
-            if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
-                return 1;
-            if (!rmax_exact) {
-                /* the verified memory bound was loose: the exact one */
-                const V rm = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax_k, bmax_k, D);
-                if (rm < 0) return -1; /* cannot be None below a verified bound */
-                rmax_exact = true;
-                mem_prev_b = bmax_k;
-                mem_prev_r = rm;
-                mem_guess = rm - bmax_k;
-                mr_ub = (V)t.p * (rm - bmax_k) + Num<V>::sc(bsum_k, q);
-                b2 = grup + mr_ub + cl;
-                if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
-                    return 1;
-            }
-            const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
-            if (r == (V)-2) return -1;
-            if (r >= 0) return 1;
-            if (!have_exact_mr) {
-                /* exact memory responses, ascending bases with warm starts */
-                tm.pfor(t.p, [&](int j) { bases[j] = Num<V>::sc(ml_hi[j] + t.B, q); });
-                tm.pfor(t.p, [&](int j) {
-                    int rk = 0;
-                    #pragma unroll 1
-                    for (int x = 0; x < t.p; x++)
-                        rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
-                    ord[rk] = j;
-                });
-                V pb = 0, pr = 0, acc = 0;
-                #pragma unroll 1
-                for (int st = 0; st < t.p; st++) {
-                    const V b = bases[ord[st]];
-                    const V r0 = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, b,
-                                          st ? tmax(b, pr + (b - pb)) : b, D);
-                    if (r0 < 0) return r0 == (V)-2 ? -1 : 0; /* cannot be None: rmax was not */
-                    acc += r0;
-                    pb = b;
-                    pr = r0;
-                }
-                sum_mr = acc;
-                have_exact_mr = true;
-            }
-            if (sum_mr != mr_ub) {
-                const V b3 = grup + sum_mr + cl;
-                const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
-                if (r3 == (V)-2) return -1;
-                if (r3 >= 0) return 1;
-            }
-        } else {
-            const V b3 = grup + cl;
-            if (RTGPU_FAST_DCHECK && b3 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, D, D, 1) >= 0)
-                return 1;
-            const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
-            if (r3 == (V)-2) return -1;
-            if (r3 >= 0) return 1;
-        }
-        /* R1 = GR up + sum MR + sum CR (analysis.py:207) */
-        if (sum_cr == -1) {
-            tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q); });
-            tm.pfor(t.m, [&](int j) {
-                int rk = 0;
-                #pragma unroll 1
-                for (int x = 0; x < t.m; x++)
-                    rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
-                ord[rk] = j;
-            });
-            V pb = 0, pr = 0, acc = 0;
-            #pragma unroll 1
-            for (int st = 0; st < t.m; st++) {
-                const V b = bases[ord[st]];
-                const V r0 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b,
-                                      st ? tmax(b, pr + (b - pb)) : b, D);
-                if (r0 == (V)-2) return -1;
-                if (r0 < 0) {
-                    acc = -2;
-                    break;
-                }
-                acc += r0;
-                pb = b;
-                pr = r0;
-            }
-            sum_cr = acc;
-        }
-        if (sum_cr < 0) return 0;
-        return grup + sum_mr + sum_cr <= D ? 1 : 0;
-    };
-    /* smallest passing count: glo, else ghi, else bisection -- one call
-     * site for `passes` keeps a single inlined copy */
-    g = 0;
-    int lo = glo, hi = ghi, phase = t.isgpu ? 0 : 3;
-    int cand = t.isgpu ? glo : 0;
-    #pragma unroll 1
-    for (;;) {
-        const int o = passes(cand);
-        if (o < 0) return -2;
-        if (phase == 3) { /* pure-CPU task: one evaluation */
-            if (!o) return -1;
-            break;
-        }
-        if (phase == 0) {
-            if (o) {
-                g = glo;
-                break;
-            }
-            if (glo >= ghi) return -1;
-            phase = 1;
-            cand = ghi;
-            continue;
-        }
-        if (phase == 1) {
-            if (!o) return -1;
-            phase = 2;
-        } else if (o) {
-            hi = cand;
-        } else {
-            lo = cand;
-        }
-        if (hi - lo <= 1) {
-            g = hi;
-            break;
-        }
-        cand = lo + (hi - lo) / 2;
-    }
-    
-    ft.mem_prev_b = mem_prev_b;
-    ft.mem_prev_r = mem_prev_r;
-    ft.mem_guess = mem_guess;
-    return g;
-}
-
 template <class V, class TM>
 RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
     typedef i64 Qt;
@@ -2353,26 +2116,205 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
             }
         }
 #endif
-        c.evals++;
+        c.evals++; /* one count evaluation per task, quick or exact */
         if (!quick) {
-            FastTask<V> ft;
-            ft.q = q;
-            ft.A = A;
-            ft.D = D;
-            ft.mem_prev_b = mem_prev_b;
-            ft.mem_prev_r = mem_prev_r;
-            ft.mem_guess = mem_guess;
-            ft.k = k;
-            ft.glo = glo;
-            ft.ghi = ghi;
-            ft.lg_tab = lg_tab;
-            const int r = fast_task_exact(tm, c, ft);
-            if (r == -1) return RTGPU_UNSCHEDULABLE;
-            if (r == -2) return ST_ESCALATE;
-            g = r;
-            mem_prev_b = ft.mem_prev_b;
-            mem_prev_r = ft.mem_prev_r;
-            mem_guess = ft.mem_guess;
+            /* ---- g-independent part: memory responses (Lemma 6) */
+            V sum_mr = 0, mr_ub = 0;
+            bool have_exact_mr = t.p == 0, rmax_exact = true;
+            i64 bsum_k = 0;
+            V bmax_k = 0;
+            if (t.p > 0) {
+                i64 bmax_t = 0, bsum_t = 0;
+    #if defined(__CUDA_ARCH__) && !defined(RTGPU_FAST_NO_LANESUMS)
+                { /* one load per lane and two butterflies (p <= 30): +1.1% on the
+                   * 8 x 5 sweep over the sequential loop (scripts/gpu_lat_ab.sh r2u) */
+                    const i64 v = tm.lane < t.p ? ml_hi[tm.lane] + t.B : 0;
+                    bmax_t = v;
+                    bsum_t = v;
+                    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        bmax_t = tmax(bmax_t, shfl_x(bmax_t, off));
+                        bsum_t += shfl_x(bsum_t, off);
+                    }
+                }
+    #else
+                #pragma unroll 1
+                for (int j = 0; j < t.p; j++) {
+                    bmax_t = tmax(bmax_t, ml_hi[j] + t.B);
+                    bsum_t += ml_hi[j] + t.B;
+                }
+    #endif
+                const V bmax = Num<V>::sc(bmax_t, q);
+                bsum_k = bsum_t;
+                bmax_k = bmax;
+                /* warm start across tasks: hp(k) grows with k, so the memory
+                 * interference of task k is pointwise >= that of any earlier
+                 * task, and lfp(b') >= lfp(b) + (b' - b) for b' >= b: the
+                 * previous task's fixed point shifted by the base difference is
+                 * below this one */
+                V rmax = -1;
+                /* off by default: on the 8 x 5 benchmark the longer code costs more
+                 * than the saved iterations (scripts/gpu_lat_ab.sh r2l: 24.4 vs
+                 * 25.5 M sets/s); the lattice path keeps it (alloc64 +14%) */
+    #ifdef RTGPU_FAST_GUESS
+                if (mem_guess > 0) {
+    #else
+                if (false) {
+    #endif
+                    /* the previous task's memory offset grown by half, verified
+                     * as a pre-fixed point in one evaluation (then the lfp is at
+                     * most f(U) <= D: every MR exists, bounded via f(U)); the
+                     * exact fixed point only if R2 needs it (lattice.cuh) */
+                    const V U = bmax + Num<V>::sc(1, q) + floor(mem_guess * 1.5);
+                    if (U <= D) rmax = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, U, D, 1);
+                    rmax_exact = rmax < 0;
+                }
+                if (rmax < 0) {
+                    V start = bmax;
+                    if (mem_prev_b >= 0 && bmax >= mem_prev_b) start = tmax(bmax, mem_prev_r + (bmax - mem_prev_b));
+                    rmax = start > D ? (V)-1 : lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax, start, D);
+                    if (rmax == (V)-2) return ST_ESCALATE;
+                    if (rmax < 0) return RTGPU_UNSCHEDULABLE; /* the longest copy's MR is None */
+                    mem_prev_b = bmax;
+                    mem_prev_r = rmax;
+                }
+                mem_guess = rmax - bmax;
+                mr_ub = (V)t.p * (rmax - bmax) + Num<V>::sc(bsum_t, q);
+            }
+            V sum_cr = -1; /* not computed yet; -2: some CR is None */
+            /* task k passes at count g?  (R2 with the MR upper bound, then exact) */
+            auto passes = [&](int g) -> int {
+                RT_COUNT(g_cnt_passes);
+                const V grup = t.isgpu ? (V)t.sInfl * (lg_tab ? outs[g - 1] : (V)(q / (2 * A * (Qt)g))) +
+                                             Num<V>::sc(t.sGL, q)
+                                       : (V)0;
+                const V cl = Num<V>::sc(t.sClu, q);
+                if (t.p > 0 || !have_exact_mr) {
+                    V b2 = grup + mr_ub + cl;
+                    /* R2 proven at the deadline itself (f(D) <= D) in one evaluation */
+                    if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
+                        return 1;
+                    if (!rmax_exact) {
+                        /* the verified memory bound was loose: the exact one */
+                        const V rm = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, bmax_k, bmax_k, D);
+                        if (rm < 0) return -1; /* cannot be None below a verified bound */
+                        rmax_exact = true;
+                        mem_prev_b = bmax_k;
+                        mem_prev_r = rm;
+                        mem_guess = rm - bmax_k;
+                        mr_ub = (V)t.p * (rm - bmax_k) + Num<V>::sc(bsum_k, q);
+                        b2 = grup + mr_ub + cl;
+                        if (RTGPU_FAST_DCHECK && b2 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, D, D, 1) >= 0)
+                            return 1;
+                    }
+                    const V r = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b2, b2, D);
+                    if (r == (V)-2) return -1;
+                    if (r >= 0) return 1;
+                    if (!have_exact_mr) {
+                        /* exact memory responses, ascending bases with warm starts */
+                        tm.pfor(t.p, [&](int j) { bases[j] = Num<V>::sc(ml_hi[j] + t.B, q); });
+                        tm.pfor(t.p, [&](int j) {
+                            int rk = 0;
+                            #pragma unroll 1
+                            for (int x = 0; x < t.p; x++)
+                                rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
+                            ord[rk] = j;
+                        });
+                        V pb = 0, pr = 0, acc = 0;
+                        #pragma unroll 1
+                        for (int st = 0; st < t.p; st++) {
+                            const V b = bases[ord[st]];
+                            const V r0 = lfp_fast(tm, tr, vm, k, K_MEM, lgM, MP, halfM, SM, b,
+                                                  st ? tmax(b, pr + (b - pb)) : b, D);
+                            if (r0 < 0) return r0 == (V)-2 ? -1 : 0; /* cannot be None: rmax was not */
+                            acc += r0;
+                            pb = b;
+                            pr = r0;
+                        }
+                        sum_mr = acc;
+                        have_exact_mr = true;
+                    }
+                    if (sum_mr != mr_ub) {
+                        const V b3 = grup + sum_mr + cl;
+                        const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
+                        if (r3 == (V)-2) return -1;
+                        if (r3 >= 0) return 1;
+                    }
+                } else {
+                    const V b3 = grup + cl;
+                    if (RTGPU_FAST_DCHECK && b3 <= D && lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, D, D, 1) >= 0)
+                        return 1;
+                    const V r3 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b3, b3, D);
+                    if (r3 == (V)-2) return -1;
+                    if (r3 >= 0) return 1;
+                }
+                /* R1 = GR up + sum MR + sum CR (analysis.py:207) */
+                if (sum_cr == -1) {
+                    tm.pfor(t.m, [&](int j) { bases[j] = Num<V>::sc(cl_hi[j], q); });
+                    tm.pfor(t.m, [&](int j) {
+                        int rk = 0;
+                        #pragma unroll 1
+                        for (int x = 0; x < t.m; x++)
+                            rk += (bases[x] < bases[j] || (bases[x] == bases[j] && x < j)) ? 1 : 0;
+                        ord[rk] = j;
+                    });
+                    V pb = 0, pr = 0, acc = 0;
+                    #pragma unroll 1
+                    for (int st = 0; st < t.m; st++) {
+                        const V b = bases[ord[st]];
+                        const V r0 = lfp_fast(tm, tr, vc, k, K_CPU, lgC, MC, halfC, SC, b,
+                                              st ? tmax(b, pr + (b - pb)) : b, D);
+                        if (r0 == (V)-2) return -1;
+                        if (r0 < 0) {
+                            acc = -2;
+                            break;
+                        }
+                        acc += r0;
+                        pb = b;
+                        pr = r0;
+                    }
+                    sum_cr = acc;
+                }
+                if (sum_cr < 0) return 0;
+                return grup + sum_mr + sum_cr <= D ? 1 : 0;
+            };
+            /* smallest passing count: glo, else ghi, else bisection -- one call
+             * site for `passes` keeps a single inlined copy */
+            g = 0;
+            int lo = glo, hi = ghi, phase = t.isgpu ? 0 : 3;
+            int cand = t.isgpu ? glo : 0;
+            #pragma unroll 1
+            for (;;) {
+                const int o = passes(cand);
+                if (o < 0) return ST_ESCALATE;
+                if (phase == 3) { /* pure-CPU task: one evaluation */
+                    if (!o) return RTGPU_UNSCHEDULABLE;
+                    break;
+                }
+                if (phase == 0) {
+                    if (o) {
+                        g = glo;
+                        break;
+                    }
+                    if (glo >= ghi) return RTGPU_UNSCHEDULABLE;
+                    phase = 1;
+                    cand = ghi;
+                    continue;
+                }
+                if (phase == 1) {
+                    if (!o) return RTGPU_UNSCHEDULABLE;
+                    phase = 2;
+                } else if (o) {
+                    hi = cand;
+                } else {
+                    lo = cand;
+                }
+                if (hi - lo <= 1) {
+                    g = hi;
+                    break;
+                }
+                cand = lo + (hi - lo) / 2;
+            }
         }
         if (!t.isgpu) continue;
         tm.sync();
