@@ -896,6 +896,42 @@ RT_HD void lat_copy_sums(const LSeq &, Seg32 ml, int p, i64 B, i64 &mx, i64 &sm)
     }
 }
 
+/* A cheap upper bound of the interference sum_{i in hp(k)} max_h W_i^h(H)
+ * of one resource (ticks), from the views alone: a window of length H meets
+ * at most floor(H / C) + 2 jobs of a regular chain (the first, partial one
+ * and those starting every C after it), each contributing at most its
+ * segments' total EP[p] -- one division per hp task instead of its walks.
+ * Exact integer floor (the divmod correction); FP64 sum of the quotients
+ * EP / s within 1e-9, which the callers' 1e-6 margins absorb. */
+RT_HD double lat_cycle_term(const LCtx &c, int i, int res, double H) {
+    const int info = c.info()[i];
+    const int p = res == K_CPU ? li_m(info) : li_p(info);
+    if (p <= 0) return 0.0;
+    const int PM = res == K_CPU ? c.L().MC : c.L().MP;
+    const double *v = (res == K_CPU ? c.VC() + (size_t)i * c.L().SC : c.VM() + (size_t)i * c.L().SM);
+    const double s = c.S()[i], C = v[p], EPp = v[PM + 1 + p];
+    double r;
+    const double q = Num<double>::divmod_inv(H * s, C, v[2 * PM + 3], r);
+    return (q + 2.0) * EPp * c.IS()[i];
+}
+#ifdef __CUDACC__
+template <int W>
+__device__ __forceinline__ double lat_cycle_bound(const LTeam<W> &tm, const LCtx &c, int k, int res, double H) {
+    double u = 0.0;
+    const int nh = c.hpn()[k];
+    for (int i = tm.lane; i < nh; i += 32) u += lat_cycle_term(c, i, res, H);
+    #pragma unroll
+    for (int off = 16; off > 0; off >>= 1) u += shfl_x(u, off);
+    return u;
+}
+#endif
+RT_HD double lat_cycle_bound(const LSeq &, const LCtx &c, int k, int res, double H) {
+    double u = 0.0;
+    const int nh = c.hpn()[k];
+    for (int i = 0; i < nh; i++) u += lat_cycle_term(c, i, res, H);
+    return u;
+}
+
 /* GR up of task i at count g (gpu.py:25 summed over its kernels) as
  * bi + bf / d, d = 2 A g */
 RT_HD LBase lat_grup(const LCtx &c, int i, int g) {
@@ -1128,15 +1164,41 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
             lat_copy_sums(tm, c.segs(k) + 2 * m + p, p, c.B()[k], bmax, bsum);
             S.bsum = bsum;
             S.lbm = LBase{bmax, 0, 1};
-            const double iu = lfp_lat(tm, lat_key(c, S.k, K_CPU), LBase{0, 0, 1}, (double)c.D()[S.k], c.D()[S.k], 2);
-            const int kk = S.k;
-            const LBase gr = lat_grup(c, kk, S.glo);
-            const double M = (double)c.D()[kk] - iu - (double)c.sClu()[kk] - (double)gr.bi - (gr.bf > 0 ? 1.0 : 0.0) -
-                             (double)S.bsum;
-            /* (any smaller offset bound leaves R2 passing: at most the deadline) */
-            const double rs = tmin(floor(M / (double)li_p(c.info()[kk])), (double)(c.D()[kk] - S.lbm.bi));
-            if (rs >= 0) {
-                const double r = lfp_lat(tm, lat_key(c, S.k, K_MEM), S.lbm, rs, c.D()[S.k], 1);
+#ifndef RTGPU_LAT_NOCYCLE
+            /* the CPU interference at D first from the cycle bound (no walks);
+             * the exact I_cpu(D) only if that leaves too little room */
+            double iu = lat_cycle_bound(tm, c, S.k, K_CPU, (double)c.D()[S.k]) + 1e-6;
+            bool iu_exact = false;
+#else
+            double iu = lfp_lat(tm, lat_key(c, S.k, K_CPU), LBase{0, 0, 1}, (double)c.D()[S.k], c.D()[S.k], 2);
+            bool iu_exact = true;
+#endif
+            double r = -1.0;
+            #pragma unroll 1
+            for (;;) {
+                const int kk = S.k;
+                const LBase gr = lat_grup(c, kk, S.glo);
+                const double M = (double)c.D()[kk] - iu - (double)c.sClu()[kk] - (double)gr.bi -
+                                 (gr.bf > 0 ? 1.0 : 0.0) - (double)S.bsum;
+                /* (any smaller offset bound leaves R2 passing: at most the deadline) */
+                const double rs = tmin(floor(M / (double)li_p(c.info()[kk])), (double)(c.D()[kk] - S.lbm.bi));
+                if (rs >= 0) {
+#ifndef RTGPU_LAT_NOCYCLE
+                    /* the memory pre-fixed point from the cycle bound, then by one evaluation */
+                    if (lat_cycle_bound(tm, c, S.k, K_MEM, (double)S.lbm.bi + rs) + 1e-6 <= rs) {
+                        RT_COUNT(g_cnt_flfp[3]);
+                        r = rs;
+                        break;
+                    }
+#endif
+                    r = lfp_lat(tm, lat_key(c, S.k, K_MEM), S.lbm, rs, c.D()[S.k], 1);
+                    if (r >= 0) break;
+                }
+                if (iu_exact) break;
+                iu = lfp_lat(tm, lat_key(c, S.k, K_CPU), LBase{0, 0, 1}, (double)c.D()[S.k], c.D()[S.k], 2);
+                iu_exact = true;
+            }
+            {
                 if (r >= 0) {
                     RT_COUNT(g_cnt_flfp[2]);
                     S.mg = r;
