@@ -88,6 +88,7 @@ RT_HD bool lb_over(const LBase &b, double N, i64 D) {
 struct LSlab {
     int maxn, MC, MP, SC, SM;
     int o_D, o_sClu, o_sInfl, o_sGL, o_B; /* i64 [maxn] */
+    int o_T, o_sMlu, o_Mx;                 /* i64 [maxn]: period, sum of copy bounds, longest copy */
     int o_s, o_invs;                       /* double [maxn]: scale s_i, 1 / s_i */
     int o_seg, o_gmin, o_g, o_info, o_hpn; /* int32 [maxn] */
     int o_vc, o_vm;                        /* double [maxn][SC], [maxn][SM] */
@@ -110,6 +111,9 @@ struct LSlab {
         o_sInfl = take(8 * maxn);
         o_sGL = take(8 * maxn);
         o_B = take(8 * maxn);
+        o_T = take(8 * maxn);
+        o_sMlu = take(8 * maxn);
+        o_Mx = take(8 * maxn);
         o_s = take(8 * maxn);
         o_invs = take(8 * maxn);
         o_seg = take(4 * maxn);
@@ -189,6 +193,9 @@ struct LCtx {
     RT_HD i64 *sInfl() const { return (i64 *)(sb() + L().o_sInfl); }
     RT_HD i64 *sGL() const { return (i64 *)(sb() + L().o_sGL); }
     RT_HD i64 *B() const { return (i64 *)(sb() + L().o_B); }
+    RT_HD i64 *T() const { return (i64 *)(sb() + L().o_T); }
+    RT_HD i64 *sMlu() const { return (i64 *)(sb() + L().o_sMlu); }
+    RT_HD i64 *Mx() const { return (i64 *)(sb() + L().o_Mx); }
     RT_HD double *S() const { return (double *)(sb() + L().o_s); }
     RT_HD double *IS() const { return (double *)(sb() + L().o_invs); }
     RT_HD int *seg() const { return (int *)(sb() + L().o_seg); }
@@ -693,6 +700,9 @@ RT_HD i64 lat_load(const LCtx &c, int i) {
     c.sInfl()[i] = infl;
     c.sGL()[i] = gls;
     c.B()[i] = mx;
+    c.T()[i] = T;
+    c.sMlu()[i] = mlu;
+    c.Mx()[i] = mx;
     int gm = 0;
     if (isgpu) {
         const i64 X = D - gls - mlu - clu;
@@ -1101,6 +1111,60 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         *(i64 *)(c.VC() + (size_t)k * c.L().SC) = b;
     });
     tm.pfor(n, [&](int k) { c.B()[k] = *(const i64 *)(c.VC() + (size_t)k * c.L().SC); });
+#ifndef RTGPU_LAT_NOALLQUICK
+    /* ---- every task at its minimum count at once (two-copy sets whose
+     * tasks all have kernels).  The quick pass's cycle bounds do not depend
+     * on the hp tasks' counts there: a CPU chain's cycle is C = T s and its
+     * segments total sClu s, a two-copy memory chain's C = T s and sMlu s,
+     * so task i's bound (floor(H s / C) + 2) EP / s is (floor(H / T_i) + 2)
+     * sClu_i (CPU) or sMlu_i (memory), exact integers.  Each task's test is
+     * then independent of the others' views: lanes test all tasks in
+     * parallel, and if every one passes at g_min, the all-minimum allocation
+     * -- the first one Algorithm 2 enumerates (analysis.py:250) -- is
+     * schedulable: that is the reference's answer, with no view built. */
+    if (c.mm == RTGPU_TWO_COPY) {
+        int *gk = c.g();
+        tm.pfor(n, [&](int k) {
+            const int inf = info[k];
+            int ok = 0;
+            if (li_gpu(inf) && li_p(inf) > 0) {
+                const int p = li_p(inf), nh = c.hpn()[k];
+                const i64 D = c.D()[k];
+                i64 iu = 0;
+                #pragma unroll 1
+                for (int i = 0; i < nh; i++) iu += (D / c.T()[i] + 2) * c.sClu()[i];
+                const LBase gr = lat_grup(c, k, c.gmin()[k]);
+                const i64 B = c.B()[k];
+                const i64 bmax = c.Mx()[k] + B, bsum = c.sMlu()[k] + (i64)p * B;
+                const i64 M = D - iu - c.sClu()[k] - gr.bi - (gr.bf > 0 ? 1 : 0) - bsum;
+                if (M >= 0) {
+                    i64 rs = M / p;
+                    if (rs > D - bmax) rs = D - bmax;
+                    if (rs >= 0) {
+                        const i64 H = bmax + rs;
+                        i64 um = 0;
+                        #pragma unroll 1
+                        for (int i = 0; i < nh && um <= rs; i++) um += (H / c.T()[i] + 2) * c.sMlu()[i];
+                        ok = um <= rs;
+                    }
+                }
+            }
+            gk[k] = ok ? c.gmin()[k] : -1;
+        });
+        bool all = true;
+        #pragma unroll 1
+        for (int k = 0; k < n; k++) all = all && gk[k] > 0;
+        if (all) {
+            RT_COUNT(g_cnt_eval);
+            evals = n;
+            tm.pfor(n, [&](int i) { vsm[i] = 2 * gk[i]; });
+            if (!bounds) return RTGPU_SCHEDULABLE;
+            const int r = lat_report(tm, c, 0, false, e2e, den);
+            return r ? r : RTGPU_SCHEDULABLE;
+        }
+        tm.pfor(n, [&](int k) { gk[k] = 0; });
+    }
+#endif
     (void)bases;
     /* The search state is warp-uniform and lives in the warp's LSt in shared
      * memory (every lane stores the same value): across the out-of-line fixed

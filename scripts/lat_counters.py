@@ -40,13 +40,13 @@ b, so, tb = concat_batches(parts)
 S = len(so) - 1
 cnt = (ctypes.c_longlong * 22)()
 lib.host_counters(cnt, 1)
-if name == "sweep8x5":  # the fast path (fast_verdict), as the fast kernel runs it
+if name == "sweep8x5" and not os.environ.get("LAT"):  # the fast path (fast_verdict), as the fast kernel runs it
     out = harness.analyze_batch(b, so, tb, flags=0, detail=False)
 else:
     out = harness.lattice_batch(b, so, tb)
 lib.host_counters(cnt, 0)
 v = list(cnt)
-names = ["interf0", "interf1", "lfp0", "R2_full_lfp", "eval", "rounds", "site_guessfail", "site_rmaxexact", "fit0", "fit1",
+names = ["interf0", "interf1", "lfp0", "R2_full_lfp", "allquick_sets", "rounds", "site_guessfail", "site_rmaxexact", "fit0", "fit1",
          "walks", "passes", "lat_lfp_cpu", "lat_lfp_mem", "lat_pre_cpu", "lat_pre_mem", "lat_it_cpu",
          "lat_it_mem", "lat_preit_cpu", "lat_preit_mem", "site_summr_chains", "site_sumcr_chains"]
 print(f"{name}: {S} sets, sched {(out['status'] == 1).sum()}, esc {(out['status'] == 99).sum()}")
