@@ -2036,6 +2036,57 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
             if (tr[i].prio > tr[k].prio) b = tmax(b, tr[i].maxMlu);
         tr[k].B = b;
     });
+#ifndef RTGPU_FAST_NOALLQUICK
+    /* ---- every task at its minimum count at once (two-copy sets whose
+     * tasks all have kernels; lattice.cuh has the derivation): per hp task
+     * the CPU / memory interference in a window H is at most
+     * (floor(H / T_i) + 2) sClu_i / sMlu_i (a regular chain meets at most
+     * floor(H / C) + 2 jobs, C = T at any count), so each task's quick test
+     * -- R2 at g_min with I_cpu(D), the longest copy's offset bound r* as a
+     * memory pre-fixed point -- needs no view.  Lanes test the tasks in
+     * parallel; if all pass, the all-minimum allocation (the first one
+     * Algorithm 2 enumerates) is schedulable. */
+    if (c.mm == RTGPU_TWO_COPY) {
+        bool ok = true;
+#ifdef __CUDA_ARCH__
+        for (int k = tm.lane; k < n; k += 32) {
+#else
+        for (int k = 0; k < n; k++) {
+#endif
+            const TaskRec &t = tr[k];
+            bool pk = false;
+            if (t.isgpu && t.p > 0) {
+                i64 iu = 0;
+                #pragma unroll 1
+                for (int i = 0; i < k; i++) iu += (t.D / tr[i].T + 2) * tr[i].sClu;
+                const i64 d = 2 * A * (i64)t.gmin;
+                const i64 gr = t.sGL + t.sInfl / d + (t.sInfl % d > 0 ? 1 : 0);
+                const i64 bmax = t.maxMlu + t.B, bsum = t.sMlu + (i64)t.p * t.B;
+                const i64 M = t.D - iu - t.sClu - gr - bsum;
+                if (M >= 0) {
+                    i64 rs = M / t.p;
+                    if (rs > t.D - bmax) rs = t.D - bmax;
+                    if (rs >= 0) {
+                        const i64 H = bmax + rs;
+                        i64 um = 0;
+                        #pragma unroll 1
+                        for (int i = 0; i < k && um <= rs; i++) um += (H / tr[i].T + 2) * tr[i].sMlu;
+                        pk = um <= rs;
+                    }
+                }
+            }
+            ok = ok && pk;
+        }
+#ifdef __CUDA_ARCH__
+        ok = __all_sync(0xffffffffu, ok);
+#endif
+        if (ok) {
+            c.evals = n;
+            tm.pfor(n, [&](int i) { vsm_out[i] = 2 * tr[i].gmin; });
+            return RTGPU_SCHEDULABLE;
+        }
+    }
+#endif
     const int lgC = c.lgC, lgM = c.lgM, halfC = c.halfC, halfM = c.halfM;
     const int SC = c.L.SC, SM = c.L.SM, MC = c.MC, MP = c.MP;
     V *vc = c.VC(), *vm = c.VM();
