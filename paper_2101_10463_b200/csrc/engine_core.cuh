@@ -286,6 +286,7 @@ struct Seg32 {
 struct TaskRec {
     i64 D, T, prio, seg;
     i64 sClu, sCll, sMlu, sMll, sGWlo, sInfl, sGL, innerCll, maxMlu, B;
+    double invT; /* 1 / T (fast path: the all-minimum pass's floor(H / T)) */
     int m, p, gmin, g;
     int isgpu, flags, idx, pad;
 };
@@ -1867,6 +1868,7 @@ RT_HD void load_task_fast_body(SetCtx<V> &c, int i) {
     t.sGL = gls;
     t.innerCll = inner;
     t.maxMlu = mx;
+    t.invT = t.T > 0 ? 1.0 / (double)t.T : 0.0;
     /* range bound and isolated-bound minimum count (analysis.py:239) */
     t.B = t.D + t.T + clu + cll + mlu + mll + gwl + gls + ih / c.A + 1;
     if (t.isgpu) {
@@ -2037,6 +2039,14 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
         tr[k].B = b;
     });
 #ifndef RTGPU_FAST_NOALLQUICK
+    /* floor(a / b) for 0 <= a, b < 2^52 from inv ~ 1 / b: an FP64 estimate
+     * and exact corrections (products below 2^53) -- no 64-bit division */
+    auto fdiv = [](i64 a, i64 b, double inv) -> i64 {
+        i64 q = (i64)((double)a * inv);
+        if (q * b > a) q--;
+        else if ((q + 1) * b <= a) q++;
+        return q;
+    };
     /* ---- every task at its minimum count at once (two-copy sets whose
      * tasks all have kernels; lattice.cuh has the derivation): per hp task
      * the CPU / memory interference in a window H is at most
@@ -2058,7 +2068,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
             if (t.isgpu && t.p > 0) {
                 i64 iu = 0;
                 #pragma unroll 1
-                for (int i = 0; i < k; i++) iu += (t.D / tr[i].T + 2) * tr[i].sClu;
+                for (int i = 0; i < k; i++) iu += (fdiv(t.D, tr[i].T, tr[i].invT) + 2) * tr[i].sClu;
                 const i64 d = 2 * A * (i64)t.gmin;
                 const i64 gr = t.sGL + t.sInfl / d + (t.sInfl % d > 0 ? 1 : 0);
                 const i64 bmax = t.maxMlu + t.B, bsum = t.sMlu + (i64)t.p * t.B;
@@ -2070,7 +2080,7 @@ RT_HD int fast_verdict(const TM &tm, SetCtx<V> &c, int32_t *vsm_out) {
                         const i64 H = bmax + rs;
                         i64 um = 0;
                         #pragma unroll 1
-                        for (int i = 0; i < k && um <= rs; i++) um += (H / tr[i].T + 2) * tr[i].sMlu;
+                        for (int i = 0; i < k && um <= rs; i++) um += (fdiv(H, tr[i].T, tr[i].invT) + 2) * tr[i].sMlu;
                         pk = um <= rs;
                     }
                 }

@@ -89,6 +89,7 @@ struct LSlab {
     int maxn, MC, MP, SC, SM;
     int o_D, o_sClu, o_sInfl, o_sGL, o_B; /* i64 [maxn] */
     int o_T, o_sMlu, o_Mx;                 /* i64 [maxn]: period, sum of copy bounds, longest copy */
+    int o_invT;                            /* double [maxn]: 1 / period */
     int o_s, o_invs;                       /* double [maxn]: scale s_i, 1 / s_i */
     int o_seg, o_gmin, o_g, o_info, o_hpn; /* int32 [maxn] */
     int o_vc, o_vm;                        /* double [maxn][SC], [maxn][SM] */
@@ -114,6 +115,7 @@ struct LSlab {
         o_T = take(8 * maxn);
         o_sMlu = take(8 * maxn);
         o_Mx = take(8 * maxn);
+        o_invT = take(8 * maxn);
         o_s = take(8 * maxn);
         o_invs = take(8 * maxn);
         o_seg = take(4 * maxn);
@@ -196,6 +198,7 @@ struct LCtx {
     RT_HD i64 *T() const { return (i64 *)(sb() + L().o_T); }
     RT_HD i64 *sMlu() const { return (i64 *)(sb() + L().o_sMlu); }
     RT_HD i64 *Mx() const { return (i64 *)(sb() + L().o_Mx); }
+    RT_HD double *invT() const { return (double *)(sb() + L().o_invT); }
     RT_HD double *S() const { return (double *)(sb() + L().o_s); }
     RT_HD double *IS() const { return (double *)(sb() + L().o_invs); }
     RT_HD int *seg() const { return (int *)(sb() + L().o_seg); }
@@ -701,6 +704,7 @@ RT_HD i64 lat_load(const LCtx &c, int i) {
     c.sGL()[i] = gls;
     c.B()[i] = mx;
     c.T()[i] = T;
+    c.invT()[i] = 1.0 / (double)T;
     c.sMlu()[i] = mlu;
     c.Mx()[i] = mx;
     int gm = 0;
@@ -1123,6 +1127,13 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
      * -- the first one Algorithm 2 enumerates (analysis.py:250) -- is
      * schedulable: that is the reference's answer, with no view built. */
     if (c.mm == RTGPU_TWO_COPY) {
+        /* floor(a / b), 0 <= a, b < 2^52, from 1 / b: estimate + exact corrections */
+        auto fdiv = [](i64 a, i64 b, double inv) -> i64 {
+            i64 q = (i64)((double)a * inv);
+            if (q * b > a) q--;
+            else if ((q + 1) * b <= a) q++;
+            return q;
+        };
         int *gk = c.g();
         tm.pfor(n, [&](int k) {
             const int inf = info[k];
@@ -1132,7 +1143,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                 const i64 D = c.D()[k];
                 i64 iu = 0;
                 #pragma unroll 1
-                for (int i = 0; i < nh; i++) iu += (D / c.T()[i] + 2) * c.sClu()[i];
+                for (int i = 0; i < nh; i++) iu += (fdiv(D, c.T()[i], c.invT()[i]) + 2) * c.sClu()[i];
                 const LBase gr = lat_grup(c, k, c.gmin()[k]);
                 const i64 B = c.B()[k];
                 const i64 bmax = c.Mx()[k] + B, bsum = c.sMlu()[k] + (i64)p * B;
@@ -1144,7 +1155,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                         const i64 H = bmax + rs;
                         i64 um = 0;
                         #pragma unroll 1
-                        for (int i = 0; i < nh && um <= rs; i++) um += (H / c.T()[i] + 2) * c.sMlu()[i];
+                        for (int i = 0; i < nh && um <= rs; i++) um += (fdiv(H, c.T()[i], c.invT()[i]) + 2) * c.sMlu()[i];
                         ok = um <= rs;
                     }
                 }
