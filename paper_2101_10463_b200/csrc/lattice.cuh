@@ -1115,6 +1115,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         *(i64 *)(c.VC() + (size_t)k * c.L().SC) = b;
     });
     tm.pfor(n, [&](int k) { c.B()[k] = *(const i64 *)(c.VC() + (size_t)k * c.L().SC); });
+    bool allq = false;
 #ifndef RTGPU_LAT_NOALLQUICK
     /* ---- every task at its minimum count at once (two-copy sets whose
      * tasks all have kernels).  The quick pass's cycle bounds do not depend
@@ -1167,13 +1168,15 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         for (int k = 0; k < n; k++) all = all && gk[k] > 0;
         if (all) {
             RT_COUNT(g_cnt_eval);
-            evals = n;
-            tm.pfor(n, [&](int i) { vsm[i] = 2 * gk[i]; });
-            if (!bounds) return RTGPU_SCHEDULABLE;
-            const int r = lat_report(tm, c, 0, false, e2e, den);
-            return r ? r : RTGPU_SCHEDULABLE;
+            if (!bounds) {
+                evals = n;
+                tm.pfor(n, [&](int i) { vsm[i] = 2 * gk[i]; });
+                return RTGPU_SCHEDULABLE;
+            }
+            allq = true; /* counts in g[]: the search is skipped, the report (one call site) follows */
+        } else {
+            tm.pfor(n, [&](int k) { gk[k] = 0; });
         }
-        tm.pfor(n, [&](int k) { gk[k] = 0; });
     }
 #endif
     (void)bases;
@@ -1194,9 +1197,9 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
     S.cwN = 0;
     S.mg = -1.0; /* the last task's memory offset (or its verified bound): the next guess */
     S.st = RTGPU_SCHEDULABLE;
-    S.evals = 0;
+    S.evals = allq ? n : 0;
     #pragma unroll 1
-    for (S.k = 0; S.k < c.n; S.k++) {
+    for (S.k = allq ? c.n : 0; S.k < c.n; S.k++) {
         if (S.k > 0) lat_view(tm, c, S.k - 1); /* counts of tasks before k are final */
         {
             const int k = S.k;
@@ -1491,7 +1494,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
     evals = S.evals;
     if (st == RTGPU_SCHEDULABLE) tm.pfor(n, [&](int i) { vsm[i] = li_gpu(c.info()[i]) ? 2 * c.g()[i] : 0; });
     if (!bounds) return st;
-    int have = n - 1;
+    int have = allq ? 0 : n - 1;
     if (st == RTGPU_UNSCHEDULABLE) {
         /* the reference reports the last allocation it tried: the
          * lexicographically largest (first GPU task takes the rest) */
