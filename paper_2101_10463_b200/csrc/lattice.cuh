@@ -90,6 +90,7 @@ struct LSlab {
     int o_D, o_sClu, o_sInfl, o_sGL, o_B; /* i64 [maxn] */
     int o_T, o_sMlu, o_Mx;                 /* i64 [maxn]: period, sum of copy bounds, longest copy */
     int o_invT;                            /* double [maxn]: 1 / period */
+    int o_prio;                            /* i64 [maxn]: priority (record word 4) */
     int o_s, o_invs;                       /* double [maxn]: scale s_i, 1 / s_i */
     int o_seg, o_gmin, o_g, o_info, o_hpn; /* int32 [maxn] */
     int o_vc, o_vm;                        /* double [maxn][SC], [maxn][SM] */
@@ -116,6 +117,7 @@ struct LSlab {
         o_sMlu = take(8 * maxn);
         o_Mx = take(8 * maxn);
         o_invT = take(8 * maxn);
+        o_prio = take(8 * maxn);
         o_s = take(8 * maxn);
         o_invs = take(8 * maxn);
         o_seg = take(4 * maxn);
@@ -199,6 +201,7 @@ struct LCtx {
     RT_HD i64 *sMlu() const { return (i64 *)(sb() + L().o_sMlu); }
     RT_HD i64 *Mx() const { return (i64 *)(sb() + L().o_Mx); }
     RT_HD double *invT() const { return (double *)(sb() + L().o_invT); }
+    RT_HD i64 *prio() const { return (i64 *)(sb() + L().o_prio); }
     RT_HD double *S() const { return (double *)(sb() + L().o_s); }
     RT_HD double *IS() const { return (double *)(sb() + L().o_invs); }
     RT_HD int *seg() const { return (int *)(sb() + L().o_seg); }
@@ -651,6 +654,7 @@ RT_HD i64 lat_load(const LCtx &c, int i) {
     const RecP r = rec_at(c.blob, i);
     const int m = (int)r[0], p = (int)r[1];
     const i64 D = r[2], T = r[3];
+    c.prio()[i] = r[4];
     const int want_p = m < 2 ? 0 : (c.mm == RTGPU_TWO_COPY ? 2 * m - 2 : m - 1);
     const bool isgpu = m > 1;
     int flags = 0;
@@ -1054,6 +1058,68 @@ RT_HD int lat_report(const TM &tm, const LCtx &c, int have_views, bool stop_at_f
     return 0;
 }
 
+/* Per-task code of lattice_set's setup scan: ST_ESCALATE (unsupported,
+ * irregular, inverted kernel, priorities out of order), the unschedulable
+ * verdict of an isolated failure (RTGPU_UNSCHEDULABLE is 0), or
+ * LAT_GO (-1): nothing decided. */
+enum { LAT_GO = -1 };
+RT_HD int lat_task_code(const LCtx &c, int k) {
+    const int fl = li_flags(c.info()[k]);
+    if (fl & (TF_UNSUP | TF_IRREG | TF_INV)) return ST_ESCALATE;
+    if (fl & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE; /* empty report */
+    if (k > 0 && c.prio()[k] < c.prio()[k - 1]) return ST_ESCALATE;
+    return LAT_GO;
+}
+#ifdef __CUDACC__
+template <int W>
+__device__ __forceinline__ int lat_setup_scan(const LTeam<W> &tm, const LCtx &c, int n, int GN, i64 &need,
+                                              i64 &vb_max, int &gtop) {
+    i64 nd = 0, vb = 0;
+    #pragma unroll 1
+    for (int base = 0; base < n; base += 32) {
+        const int k = base + tm.lane;
+        int ck = LAT_GO;
+        if (k < n) {
+            ck = lat_task_code(c, k);
+            if (li_gpu(c.info()[k])) nd += c.gmin()[k];
+            vb = tmax(vb, *(const i64 *)(c.VC() + (size_t)k * c.L().SC));
+        }
+        const unsigned bad = __ballot_sync(0xffffffffu, ck != LAT_GO);
+        if (bad) return __shfl_sync(0xffffffffu, ck, __ffs(bad) - 1);
+    }
+    #pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        nd += shfl_x(nd, off);
+        vb = tmax(vb, shfl_x(vb, off));
+    }
+    need = nd;
+    vb_max = vb;
+    if (need > GN) return RTGPU_UNSCHEDULABLE; /* no allocation at all: empty report */
+    int gt = 1;
+    for (int k = tm.lane; k < n; k += 32)
+        if (li_gpu(c.info()[k])) gt = tmax(gt, (int)tmin((i64)GN, (i64)c.gmin()[k] + (GN - need)));
+    #pragma unroll
+    for (int off = 16; off > 0; off >>= 1) gt = tmax(gt, __shfl_xor_sync(0xffffffffu, gt, off));
+    gtop = gt;
+    return LAT_GO;
+}
+#endif
+RT_HD int lat_setup_scan(const LSeq &, const LCtx &c, int n, int GN, i64 &need, i64 &vb_max, int &gtop) {
+    need = 0;
+    vb_max = 0;
+    for (int k = 0; k < n; k++) {
+        const int ck = lat_task_code(c, k);
+        if (ck != LAT_GO) return ck;
+        if (li_gpu(c.info()[k])) need += c.gmin()[k];
+        vb_max = tmax(vb_max, *(const i64 *)(c.VC() + (size_t)k * c.L().SC));
+    }
+    if (need > GN) return RTGPU_UNSCHEDULABLE;
+    gtop = 1;
+    for (int k = 0; k < n; k++)
+        if (li_gpu(c.info()[k])) gtop = tmax(gtop, (int)tmin((i64)GN, (i64)c.gmin()[k] + (GN - need)));
+    return LAT_GO;
+}
+
 /* The whole RTGPU analysis of one compact blob: status, allocation (vsm),
  * the number of task evaluations, and with `bounds` the report's end-to-end
  * bounds (e2e / den, else unused). */
@@ -1080,21 +1146,14 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
     });
     const int *info = c.info();
     i64 need = 0, vb_max = 0;
-    /* reference order: the first task whose minimum-count search raises or fails */
-    #pragma unroll 1
-    for (int k = 0; k < n; k++) {
-        const int fl = li_flags(info[k]);
-        if (fl & (TF_UNSUP | TF_IRREG | TF_INV)) return ST_ESCALATE;
-        if (fl & TF_ISOFAIL) return RTGPU_UNSCHEDULABLE; /* empty report */
-        if (li_gpu(info[k])) need += c.gmin()[k];
-        vb_max = tmax(vb_max, *(const i64 *)(c.VC() + (size_t)k * c.L().SC));
-        if (k > 0 && rec_at(h, k)[4] < rec_at(h, k - 1)[4]) return ST_ESCALATE;
-    }
-    if (need > GN) return RTGPU_UNSCHEDULABLE; /* no allocation at all: empty report */
     int gtop = 1;
-    #pragma unroll 1
-    for (int k = 0; k < n; k++)
-        if (li_gpu(info[k])) gtop = tmax(gtop, (int)tmin((i64)GN, (i64)c.gmin()[k] + (GN - need)));
+    {
+        /* reference order: the first task whose minimum-count search raises
+         * or fails decides; then the minimum counts' sum, the range bound
+         * and gtop -- lane-parallel, one ballot per 32 tasks */
+        const int code = lat_setup_scan(tm, c, n, GN, need, vb_max, gtop);
+        if (code != LAT_GO) return code;
+    }
     /* every value at any scale s_i <= 2 gtop below 2^51 (room for the
      * half-tick marker); the window fraction bf * s_i below 2^52 */
     if ((i128)vb_max * range_factor(n, c.L().MC, c.L().MP) * (2 * gtop) >= ((i128)1 << 51)) return ST_ESCALATE;
@@ -1104,14 +1163,14 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
      * task's longest copy until the barrier) */
     i64 *bases = c.bases();
     tm.pfor(n, [&](int k) {
-        const i64 pk = rec_at(h, k)[4];
+        const i64 pk = c.prio()[k];
         int first = k;
-        while (first > 0 && rec_at(h, first - 1)[4] == pk) first--;
+        while (first > 0 && c.prio()[first - 1] == pk) first--;
         c.hpn()[k] = first;
         i64 b = 0;
         #pragma unroll 1
         for (int i = k + 1; i < n; i++)
-            if (rec_at(h, i)[4] > pk) b = tmax(b, c.B()[i]);
+            if (c.prio()[i] > pk) b = tmax(b, c.B()[i]);
         *(i64 *)(c.VC() + (size_t)k * c.L().SC) = b;
     });
     tm.pfor(n, [&](int k) { c.B()[k] = *(const i64 *)(c.VC() + (size_t)k * c.L().SC); });
