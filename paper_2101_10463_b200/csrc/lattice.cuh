@@ -1154,10 +1154,6 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         const int code = lat_setup_scan(tm, c, n, GN, need, vb_max, gtop);
         if (code != LAT_GO) return code;
     }
-    /* every value at any scale s_i <= 2 gtop below 2^51 (room for the
-     * half-tick marker); the window fraction bf * s_i below 2^52 */
-    if ((i128)vb_max * range_factor(n, c.L().MC, c.L().MP) * (2 * gtop) >= ((i128)1 << 51)) return ST_ESCALATE;
-    if ((i128)4 * A * gtop * gtop >= ((i128)1 << 52)) return ST_ESCALATE;
     /* hp(k) = [0, first index of k's priority); blocking term of
      * analysis.py:162 = longest copy of a lower-priority task (B[] holds each
      * task's longest copy until the barrier) */
@@ -1189,6 +1185,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
     if (c.mm == RTGPU_TWO_COPY) {
         /* floor(a / b), 0 <= a, b < 2^52, from 1 / b: estimate + exact corrections */
         auto fdiv = [](i64 a, i64 b, double inv) -> i64 {
+            if ((a | b) >= ((i64)1 << 52)) return a / b; /* beyond the exact FP64 estimate */
             i64 q = (i64)((double)a * inv);
             if (q * b > a) q--;
             else if ((q + 1) * b <= a) q++;
@@ -1203,7 +1200,7 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                 const i64 D = c.D()[k];
                 i64 iu = 0;
                 #pragma unroll 1
-                for (int i = 0; i < nh; i++) iu += (fdiv(D, c.T()[i], c.invT()[i]) + 2) * c.sClu()[i];
+                for (int i = 0; i < nh && iu <= D; i++) iu += (fdiv(D, c.T()[i], c.invT()[i]) + 2) * c.sClu()[i];
                 const LBase gr = lat_grup(c, k, c.gmin()[k]);
                 const i64 B = c.B()[k];
                 const i64 bmax = c.Mx()[k] + B, bsum = c.sMlu()[k] + (i64)p * B;
@@ -1238,6 +1235,15 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
         }
     }
 #endif
+    /* the search and the report run on FP64 views: every value at any scale
+     * s_i <= 2 gtop below 2^51 (room for the half-tick marker), the window
+     * fraction bf * s_i below 2^52 (the all-minimum pass above is integer
+     * arithmetic and takes any range the loads accept) */
+    if ((i128)vb_max * range_factor(n, c.L().MC, c.L().MP) * (2 * gtop) >= ((i128)1 << 51) ||
+        (i128)4 * A * gtop * gtop >= ((i128)1 << 52)) {
+        if (allq) tm.pfor(n, [&](int k) { c.g()[k] = 0; });
+        return ST_ESCALATE;
+    }
     (void)bases;
     /* The search state is warp-uniform and lives in the warp's LSt in shared
      * memory (every lane stores the same value): across the out-of-line fixed
