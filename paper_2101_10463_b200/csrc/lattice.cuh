@@ -1502,8 +1502,9 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
             S.g = 0;
             S.lo = S.glo;
             S.hi = S.ghi;
-            S.phase = gpu ? 0 : 3;
-            S.cand = gpu ? S.glo : 0;
+            /* the largest count first (fast path: engine_core.cuh) */
+            S.phase = gpu ? 1 : 3;
+            S.cand = gpu ? S.ghi : 0;
             S.fail = 0;
         }
         #pragma unroll 1
@@ -1515,22 +1516,22 @@ RT_HD int lattice_set(const TM &tm, LCtx &c, bool bounds, int32_t *vsm, i64 *e2e
                 S.fail = !o;
                 break;
             }
-            if (phase == 0) {
-                if (o) {
-                    S.g = S.glo;
-                    break;
-                }
-                if (S.glo >= S.ghi) {
-                    S.fail = 1;
-                    break;
-                }
-                S.phase = 1;
-                S.cand = S.ghi;
-                continue;
-            }
             if (phase == 1) {
                 if (!o) {
                     S.fail = 1;
+                    break;
+                }
+                if (S.glo >= S.ghi) {
+                    S.g = S.ghi;
+                    break;
+                }
+                S.phase = 0;
+                S.cand = S.glo;
+                continue;
+            }
+            if (phase == 0) {
+                if (o) {
+                    S.g = S.glo;
                     break;
                 }
                 S.phase = 2;
